@@ -1,0 +1,136 @@
+/*
+ * include/na.h — C ABI of the B200 fused neighborhood attention library
+ * (libna.so, built from paper_2403_04690_b200/csrc for sm_100a).
+ *
+ * The operation (PAPER.md = /root/reference/PAPER.md, cited as P:line):
+ *   Eq. 1, scaled dot-product attention, restricted per query x
+ *   to its neighborhood N(x) (Fig. 2 caption):
+ *     O_x   = sum_{y in N(x)} softmax_y(scale <q_x, k_y>) v_y
+ *     LSE_x = log sum_{y in N(x)} exp(scale <q_x, k_y>)      (natural log)
+ *   N(x) is the Cartesian product over axes a of a per-axis window: the
+ *   query's residue class r = x_a mod dilation_a is treated as a
+ *   non-dilated axis of ceil((L_a - r)/dilation_a) tokens (§3.4);
+ *   on it the window holds kernel_size_a consecutive members, centred on the
+ *   query and shifted inward at the borders, or, on a
+ *   causal axis, the kernel_size_a members ending at the query (P:117-118,
+ *   P:332-334).  See DESIGN.md "Readings" for every choice the paper leaves
+ *   open (window placement rule, even kernels, LSE base, tolerances ...).
+ *   The forward is fused (§3.3): attention weights never reach
+ *   global memory.  The backward (§3.1 operators PN/NN/IN)
+ *   recomputes the weights from LSE and writes dQ, dK, dV with exactly one
+ *   writer per element (no atomics).
+ *
+ * Conventions (all entry points):
+ *   - Tensors Q, K, V, O, dO, dQ, dK, dV are DEVICE pointers to contiguous
+ *     [batch, heads, X0 (, X1 (, X2)), head_dim] arrays of `dtype`
+ *     (X0 outermost; e.g. T, H, W for video).  LSE is a device pointer to a
+ *     contiguous fp32 [batch, heads, X0 (, X1 (, X2))] array.  All base
+ *     pointers must be 16-byte aligned.
+ *   - The caller owns every buffer; the library never allocates device
+ *     memory.  The backward workspace is caller-supplied.
+ *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t;
+ *     0 = legacy default stream).  Buffers must stay live until the stream
+ *     reaches the call.
+ *   - The problem is validated before anything is launched.  On any error
+ *     nothing is launched and nothing is written; the status is returned
+ *     (never thrown, never abort()).  na_last_error() gives a thread-local
+ *     detail string for the last failing call on this thread.
+ *   - Results are deterministic: identical inputs on the same device give
+ *     bitwise identical outputs.
+ *   - Thread safety: entry points may be called concurrently from several
+ *     host threads.
+ *   - Multi-GPU is not part of the ABI: callers shard batch x heads and call
+ *     the library once per device.
+ */
+#ifndef NA_H_
+#define NA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { NA_F32 = 0, NA_F16 = 1, NA_BF16 = 2 } na_dtype;
+
+typedef enum {
+  NA_OK = 0,
+  NA_ERR_NULL = 1,            /* null problem or required tensor pointer                  */
+  NA_ERR_RANK = 2,            /* rank not in {1,2,3}         */
+  NA_ERR_SHAPE = 3,           /* batch, heads, head_dim or an extent < 1                   */
+  NA_ERR_BAD_KERNEL = 4,      /* kernel_size < 1                                           */
+  NA_ERR_EVEN_WINDOW = 5,     /* even kernel_size on a non-causal axis  */
+  NA_ERR_BAD_DILATION = 6,    /* dilation < 1         */
+  NA_ERR_WINDOW_EXCEEDS = 7,  /* kernel_size * dilation > extent: the window would not fit
+                                 in the smallest residue class  */
+  NA_ERR_DTYPE = 8,           /* dtype not one of na_dtype                                 */
+  NA_ERR_HEAD_DIM = 9,        /* head_dim > 256 or not a multiple of 8 (16-bit) / 4 (fp32) */
+  NA_ERR_ALIGNMENT = 10,      /* a tensor base pointer is not 16-byte aligned              */
+  NA_ERR_LAYOUT = 11,         /* non-contiguous strides requested (not supported)          */
+  NA_ERR_WORKSPACE = 12,      /* backward workspace missing or smaller than required       */
+  NA_ERR_CUDA = 13,           /* CUDA launch/driver error (see na_last_error)              */
+  NA_ERR_IMPL = 14            /* the requested `impl` cannot run this problem              */
+} na_status;
+
+/* Kernel family selection (tests and benchmarks use it to pin a path). */
+typedef enum {
+  NA_IMPL_AUTO = 0,  /* tensor-core path when the problem fits it, else SIMT  */
+  NA_IMPL_SIMT = 1,  /* fp32 CUDA-core kernels (any dtype; fp32 inputs always) */
+  NA_IMPL_TC = 2     /* tcgen05 + TMEM + TMA kernels (fp16 / bf16 only)        */
+} na_impl;
+
+typedef struct {
+  int32_t rank;            /* 1..3 spatial axes                                   */
+  int32_t batch, heads;    /* >= 1                                                */
+  int32_t head_dim;        /* d in Eq. 1                                          */
+  int32_t extent[3];       /* L_a, outermost axis first; entries >= rank ignored  */
+  int32_t kernel_size[3];  /* k_a: window size per axis        */
+  int32_t dilation[3];     /* dilation_a >= 1                  */
+  int32_t is_causal[3];    /* 0/1 per axis                 */
+  float scale;             /* softmax scale; <= 0 means 1/sqrt(head_dim)  */
+  na_dtype dtype;          /* of Q,K,V,O,dO,dQ,dK,dV; LSE/workspace always fp32   */
+  na_impl impl;            /* NA_IMPL_AUTO unless pinning a kernel family         */
+  const int64_t* strides;  /* must be NULL (contiguous); else NA_ERR_LAYOUT       */
+} na_problem;
+
+/* Validates `p` alone (no pointers).  Pure host function; never touches a GPU. */
+na_status na_validate(const na_problem* p);
+
+/* Forward.  Reads q, k, v; writes o and, if lse != NULL, lse (fp32 natural-log
+ * LSE_x, needed by na_bwd).  One kernel launch on `stream`. */
+na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* v, void* o,
+                 float* lse, void* stream);
+
+/* Bytes of device workspace na_bwd needs: batch*heads*prod(extent)*4
+ * (the fp32 row vector D_x = <dO_x, O_x>). */
+size_t na_bwd_workspace_size(const na_problem* p);
+
+/* Backward.  Reads q, k, v, o, d_o (dL/dO) and lse from na_fwd on the same
+ * inputs; writes dq, dk, dv (each element by exactly one thread; no
+ * atomics).  `workspace` (device, >= na_bwd_workspace_size bytes) is
+ * scratch owned by the caller.  Three launches on `stream`:
+ * D_x = <dO_x, O_x>, then dK/dV (key-stationary, inverse neighborhood map),
+ * then dQ (query-stationary, forward map). */
+na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* v,
+                 const void* o, const void* d_o, const float* lse, void* dq, void* dk,
+                 void* dv, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Which kernel family na_fwd/na_bwd would run for `p` (NA_IMPL_SIMT or
+ * NA_IMPL_TC), or -1 if `p` is invalid.  Host only. */
+int na_selected_impl(const na_problem* p);
+
+/* Static description of a status code. */
+const char* na_status_string(na_status s);
+
+/* Detail message of the last failing call on this host thread ("" if none). */
+const char* na_last_error(void);
+
+/* Number of kernel launches the last successful na_fwd / na_bwd issued on
+ * this host thread (for the benchmark's gpu_launches count). */
+int na_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NA_H_ */

@@ -1,0 +1,345 @@
+// fna_simt.cu — CUDA-core (fp32 FFMA) fused neighborhood attention kernels.
+//
+// The fp32 path of the library (TF32 off, so fp32 problems meet the 1e-4
+// tolerance) and the path for any problem the tcgen05 kernels do not cover.
+// One warp per output row: the 32 lanes split head_dim, the warp walks the
+// row's neighborhood key by key with an online softmax (Milakov-Gimelshein,
+// P:152-156) so attention weights never leave registers (fused, §3.3).
+//
+//   fna_fwd_simt    : O_x, LSE_x for every query x         (Eq. 1)
+//   fna_bwd_pre     : D_x = <dO_x, O_x>                      (softmax Jacobian)
+//   fna_dq_simt     : dQ_x = scale sum_y P(dP - D_x) k_y     (NN on dA)
+//   fna_dkdv_simt   : dK_y, dV_y over the inverse window     (IN)
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "na_geom.cuh"
+#include "na_kernels.h"
+
+namespace na {
+namespace {
+
+template <typename T> __device__ __forceinline__ float ld(const T* p);
+template <> __device__ __forceinline__ float ld<float>(const float* p) { return __ldg(p); }
+template <> __device__ __forceinline__ float ld<__half>(const __half* p) { return __half2float(__ldg(p)); }
+template <> __device__ __forceinline__ float ld<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(__ldg(p));
+}
+template <typename T> __device__ __forceinline__ T cvt(float x);
+template <> __device__ __forceinline__ float cvt<float>(float x) { return x; }
+template <> __device__ __forceinline__ __half cvt<__half>(float x) { return __float2half_rn(x); }
+template <> __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Per-axis compacted coordinate, residue and class size of flat token x.
+struct Coord {
+  int c[3], r[3], Lr[3];
+};
+
+__device__ __forceinline__ Coord decode(const Geom& g, int x) {
+  Coord o;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    int v = a < g.rank ? (x / g.tstride[a]) % g.L[a] : 0;
+    int dil = g.dil[a];
+    o.r[a] = v % dil;
+    o.c[a] = v / dil;
+    o.Lr[a] = a < g.rank ? class_size(g.L[a], dil, o.r[a]) : 1;
+  }
+  return o;
+}
+
+__device__ __forceinline__ int token_of(const Geom& g, const Coord& co, const int cc[3]) {
+  int t = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (a < g.rank) t += (co.r[a] + g.dil[a] * cc[a]) * g.tstride[a];
+  return t;
+}
+
+// ------------------------------------------------------------------ forward
+template <typename T, int DPL>
+__global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict__ q,
+                                                    const T* __restrict__ k,
+                                                    const T* __restrict__ v, T* __restrict__ o,
+                                                    float* __restrict__ lse) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= (int64_t)g.BH * g.N) return;
+  const int bh = (int)(row / g.N), x = (int)(row % g.N);
+  const int64_t base = (int64_t)bh * g.N * g.D;
+  float qr[DPL], acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    int d = lane + 32 * i;
+    qr[i] = d < g.D ? ld(q + base + (int64_t)x * g.D + d) * g.scale_log2 : 0.f;
+    acc[i] = 0.f;
+  }
+  const Coord co = decode(g, x);
+  int lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = a < g.rank ? win_start(co.c[a], co.Lr[a], g.k[a], g.causal[a]) : 0;
+    hi[a] = a < g.rank ? win_end(co.c[a], co.Lr[a], g.k[a], g.causal[a]) : 0;
+  }
+  float m = -INFINITY, l = 0.f;
+  int cc[3];
+  for (cc[0] = lo[0]; cc[0] <= hi[0]; ++cc[0])
+    for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
+      for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
+        const int64_t y = base + (int64_t)token_of(g, co, cc) * g.D;
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          int d = lane + 32 * i;
+          if (d < g.D) s = fmaf(qr[i], ld(k + y + d), s);
+        }
+        s = warp_sum(s);                       // log2-domain logit
+        const float mn = fmaxf(m, s);
+        const float corr = exp2f(m - mn);      // 0 when m = -inf
+        const float p = exp2f(s - mn);
+        l = l * corr + p;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          int d = lane + 32 * i;
+          acc[i] = acc[i] * corr + (d < g.D ? p * ld(v + y + d) : 0.f);
+        }
+        m = mn;
+      }
+  const float inv = 1.f / l;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    int d = lane + 32 * i;
+    if (d < g.D) o[base + (int64_t)x * g.D + d] = cvt<T>(acc[i] * inv);
+  }
+  if (lse && lane == 0) lse[row] = (m + log2f(l)) * 0.69314718055994531f;
+}
+
+// ------------------------------------------------------------- bwd: D_x
+template <typename T>
+__global__ void __launch_bounds__(256) fna_bwd_pre(Geom g, const T* __restrict__ o,
+                                                   const T* __restrict__ d_o,
+                                                   float* __restrict__ Dvec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= (int64_t)g.BH * g.N) return;
+  float s = 0.f;
+  for (int d = lane; d < g.D; d += 32) s = fmaf(ld(o + row * g.D + d), ld(d_o + row * g.D + d), s);
+  s = warp_sum(s);
+  if (lane == 0) Dvec[row] = s;
+}
+
+// ------------------------------------------------------------- bwd: dQ
+template <typename T, int DPL>
+__global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__ q,
+                                                   const T* __restrict__ k,
+                                                   const T* __restrict__ v,
+                                                   const T* __restrict__ d_o,
+                                                   const float* __restrict__ lse,
+                                                   const float* __restrict__ Dvec,
+                                                   T* __restrict__ dq) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= (int64_t)g.BH * g.N) return;
+  const int bh = (int)(row / g.N), x = (int)(row % g.N);
+  const int64_t base = (int64_t)bh * g.N * g.D;
+  float qr[DPL], dor[DPL], acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    int d = lane + 32 * i;
+    qr[i] = d < g.D ? ld(q + base + (int64_t)x * g.D + d) : 0.f;
+    dor[i] = d < g.D ? ld(d_o + base + (int64_t)x * g.D + d) : 0.f;
+    acc[i] = 0.f;
+  }
+  const float lse_x = lse[row], D_x = Dvec[row];
+  const Coord co = decode(g, x);
+  int lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = a < g.rank ? win_start(co.c[a], co.Lr[a], g.k[a], g.causal[a]) : 0;
+    hi[a] = a < g.rank ? win_end(co.c[a], co.Lr[a], g.k[a], g.causal[a]) : 0;
+  }
+  int cc[3];
+  for (cc[0] = lo[0]; cc[0] <= hi[0]; ++cc[0])
+    for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
+      for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
+        const int64_t y = base + (int64_t)token_of(g, co, cc) * g.D;
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          int d = lane + 32 * i;
+          if (d < g.D) {
+            s = fmaf(qr[i], ld(k + y + d), s);
+            dp = fmaf(dor[i], ld(v + y + d), dp);
+          }
+        }
+        s = warp_sum(s);
+        dp = warp_sum(dp);
+        const float p = __expf(s * g.scale - lse_x);
+        const float ds = p * (dp - D_x);
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          int d = lane + 32 * i;
+          if (d < g.D) acc[i] = fmaf(ds, ld(k + y + d), acc[i]);
+        }
+      }
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    int d = lane + 32 * i;
+    if (d < g.D) dq[base + (int64_t)x * g.D + d] = cvt<T>(acc[i] * g.scale);
+  }
+}
+
+// ------------------------------------------------------------- bwd: dK, dV
+template <typename T, int DPL>
+__global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, const T* __restrict__ q,
+                                                     const T* __restrict__ k,
+                                                     const T* __restrict__ v,
+                                                     const T* __restrict__ d_o,
+                                                     const float* __restrict__ lse,
+                                                     const float* __restrict__ Dvec,
+                                                     T* __restrict__ dk, T* __restrict__ dv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= (int64_t)g.BH * g.N) return;
+  const int bh = (int)(row / g.N), y = (int)(row % g.N);
+  const int64_t base = (int64_t)bh * g.N * g.D;
+  float kr[DPL], vr[DPL], ak[DPL], av[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    int d = lane + 32 * i;
+    kr[i] = d < g.D ? ld(k + base + (int64_t)y * g.D + d) : 0.f;
+    vr[i] = d < g.D ? ld(v + base + (int64_t)y * g.D + d) : 0.f;
+    ak[i] = av[i] = 0.f;
+  }
+  const Coord co = decode(g, y);
+  int lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {   // inverse neighborhood: exact per-axis intervals
+    lo[a] = a < g.rank ? inv_start(co.c[a], co.Lr[a], g.k[a], g.causal[a]) : 0;
+    hi[a] = a < g.rank ? inv_end(co.c[a], co.Lr[a], g.k[a], g.causal[a]) : 0;
+  }
+  int cc[3];
+  for (cc[0] = lo[0]; cc[0] <= hi[0]; ++cc[0])
+    for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
+      for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
+        const int xt = token_of(g, co, cc);
+        const int64_t xo = base + (int64_t)xt * g.D;
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          int d = lane + 32 * i;
+          if (d < g.D) {
+            s = fmaf(ld(q + xo + d), kr[i], s);
+            dp = fmaf(ld(d_o + xo + d), vr[i], dp);
+          }
+        }
+        s = warp_sum(s);
+        dp = warp_sum(dp);
+        const int64_t xr = (int64_t)bh * g.N + xt;
+        const float p = __expf(s * g.scale - lse[xr]);
+        const float ds = p * (dp - Dvec[xr]);
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          int d = lane + 32 * i;
+          if (d < g.D) {
+            ak[i] = fmaf(ds, ld(q + xo + d), ak[i]);
+            av[i] = fmaf(p, ld(d_o + xo + d), av[i]);
+          }
+        }
+      }
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    int d = lane + 32 * i;
+    if (d < g.D) {
+      dk[base + (int64_t)y * g.D + d] = cvt<T>(ak[i] * g.scale);
+      dv[base + (int64_t)y * g.D + d] = cvt<T>(av[i]);
+    }
+  }
+}
+
+template <typename T, int DPL>
+cudaError_t launch_fwd(const Geom& g, const void* q, const void* k, const void* v, void* o,
+                       float* lse, cudaStream_t st) {
+  const int64_t rows = (int64_t)g.BH * g.N;
+  fna_fwd_simt<T, DPL><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+      g, (const T*)q, (const T*)k, (const T*)v, (T*)o, lse);
+  return cudaGetLastError();
+}
+
+template <typename T, int DPL>
+cudaError_t launch_bwd(const Geom& g, const void* q, const void* k, const void* v, const void* o,
+                       const void* d_o, const float* lse, void* dq, void* dk, void* dv,
+                       float* Dvec, cudaStream_t st) {
+  const int64_t rows = (int64_t)g.BH * g.N;
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  fna_bwd_pre<T><<<grid, 256, 0, st>>>(g, (const T*)o, (const T*)d_o, Dvec);
+  fna_dkdv_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
+                                              (const T*)d_o, lse, Dvec, (T*)dk, (T*)dv);
+  fna_dq_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
+                                            (const T*)d_o, lse, Dvec, (T*)dq);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t fwd_by_dim(const Geom& g, const void* q, const void* k, const void* v, void* o,
+                       float* lse, cudaStream_t st) {
+  if (g.D <= 32) return launch_fwd<T, 1>(g, q, k, v, o, lse, st);
+  if (g.D <= 64) return launch_fwd<T, 2>(g, q, k, v, o, lse, st);
+  if (g.D <= 128) return launch_fwd<T, 4>(g, q, k, v, o, lse, st);
+  return launch_fwd<T, 8>(g, q, k, v, o, lse, st);
+}
+
+template <typename T>
+cudaError_t bwd_by_dim(const Geom& g, const void* q, const void* k, const void* v, const void* o,
+                       const void* d_o, const float* lse, void* dq, void* dk, void* dv,
+                       float* Dvec, cudaStream_t st) {
+  if (g.D <= 32) return launch_bwd<T, 1>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+  if (g.D <= 64) return launch_bwd<T, 2>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+  if (g.D <= 128) return launch_bwd<T, 4>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+  return launch_bwd<T, 8>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+}
+
+}  // namespace
+
+cudaError_t simt_fwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+                     void* o, float* lse, cudaStream_t st) {
+  switch (dtype) {
+    case 0: return fwd_by_dim<float>(g, q, k, v, o, lse, st);
+    case 1: return fwd_by_dim<__half>(g, q, k, v, o, lse, st);
+    default: return fwd_by_dim<__nv_bfloat16>(g, q, k, v, o, lse, st);
+  }
+}
+
+cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, float* Dvec,
+                           cudaStream_t st) {
+  const int64_t rows = (int64_t)g.BH * g.N;
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  switch (dtype) {
+    case 0: fna_bwd_pre<float><<<grid, 256, 0, st>>>(g, (const float*)o, (const float*)d_o, Dvec); break;
+    case 1: fna_bwd_pre<__half><<<grid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec); break;
+    default:
+      fna_bwd_pre<__nv_bfloat16><<<grid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
+                                                       (const __nv_bfloat16*)d_o, Dvec);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t simt_bwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+                     const void* o, const void* d_o, const float* lse, void* dq, void* dk,
+                     void* dv, float* Dvec, cudaStream_t st) {
+  switch (dtype) {
+    case 0: return bwd_by_dim<float>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+    case 1: return bwd_by_dim<__half>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+    default: return bwd_by_dim<__nv_bfloat16>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+  }
+}
+
+}  // namespace na

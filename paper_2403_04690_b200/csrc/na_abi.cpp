@@ -1,0 +1,221 @@
+// na_abi.cpp — the C ABI of libna.so (include/na.h): validation, kernel-family
+// selection and launch.  Everything here is host code; the arithmetic runs in
+// the CUDA kernels (fna_simt.cu, fna_tc_fwd.cu, fna_tc_bwd.cu).
+#include "../../include/na.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "na_kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_last_launches = 0;
+
+na_status fail(na_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+// Constraint list of S:62-70 / S:132-137 plus the ABI's own limits.
+na_status validate(const na_problem* p) {
+  if (!p) return fail(NA_ERR_NULL, "problem is NULL");
+  if (p->rank < 1 || p->rank > 3) return fail(NA_ERR_RANK, "rank %d not in {1,2,3}", p->rank);
+  if (p->batch < 1 || p->heads < 1 || p->head_dim < 1)
+    return fail(NA_ERR_SHAPE, "batch/heads/head_dim must be >= 1");
+  int64_t n = 1;
+  for (int a = 0; a < p->rank; ++a) {
+    if (p->extent[a] < 1) return fail(NA_ERR_SHAPE, "extent[%d] = %d < 1", a, p->extent[a]);
+    if (p->kernel_size[a] < 1)
+      return fail(NA_ERR_BAD_KERNEL, "kernel_size[%d] = %d < 1", a, p->kernel_size[a]);
+    if (!p->is_causal[a] && p->kernel_size[a] % 2 == 0)
+      return fail(NA_ERR_EVEN_WINDOW, "even kernel_size[%d] = %d on a non-causal axis", a,
+                  p->kernel_size[a]);
+    if (p->dilation[a] < 1)
+      return fail(NA_ERR_BAD_DILATION, "dilation[%d] = %d < 1", a, p->dilation[a]);
+    if ((int64_t)p->kernel_size[a] * p->dilation[a] > p->extent[a])
+      return fail(NA_ERR_WINDOW_EXCEEDS,
+                  "kernel_size[%d]*dilation[%d] = %lld > extent %d (window exceeds the "
+                  "smallest residue class)",
+                  a, a, (long long)p->kernel_size[a] * p->dilation[a], p->extent[a]);
+    n *= p->extent[a];
+  }
+  if (p->dtype != NA_F32 && p->dtype != NA_F16 && p->dtype != NA_BF16)
+    return fail(NA_ERR_DTYPE, "dtype %d unknown", (int)p->dtype);
+  const int align = p->dtype == NA_F32 ? 4 : 8;   // rows must be 16-byte multiples
+  if (p->head_dim > 256 || p->head_dim % align)
+    return fail(NA_ERR_HEAD_DIM, "head_dim %d: need <= 256 and a multiple of %d", p->head_dim,
+                align);
+  if (p->strides) return fail(NA_ERR_LAYOUT, "only contiguous [B,H,X...,D] is supported");
+  if ((int64_t)p->batch * p->heads * n * p->head_dim > (int64_t(1) << 40))
+    return fail(NA_ERR_SHAPE, "problem too large");
+  if ((int64_t)p->batch * p->heads > 0x7fffffff || n > 0x7fffffff)
+    return fail(NA_ERR_SHAPE, "B*H or tokens exceed int32");
+  if (p->impl != NA_IMPL_AUTO && p->impl != NA_IMPL_SIMT && p->impl != NA_IMPL_TC)
+    return fail(NA_ERR_IMPL, "impl %d unknown", (int)p->impl);
+  return NA_OK;
+}
+
+na::Geom make_geom(const na_problem* p) {
+  na::Geom g{};
+  g.rank = p->rank;
+  g.BH = p->batch * p->heads;
+  g.D = p->head_dim;
+  int n = 1;
+  for (int a = 0; a < 3; ++a) {
+    bool on = a < p->rank;
+    g.L[a] = on ? p->extent[a] : 1;
+    g.k[a] = on ? p->kernel_size[a] : 1;
+    g.dil[a] = on ? p->dilation[a] : 1;
+    g.causal[a] = on ? (p->is_causal[a] ? 1 : 0) : 0;
+    n *= g.L[a];
+  }
+  g.N = n;
+  int s = 1;
+  for (int a = p->rank - 1; a >= 0; --a) {
+    g.tstride[a] = s;
+    s *= g.L[a];
+  }
+  for (int a = p->rank; a < 3; ++a) g.tstride[a] = 1;
+  g.scale = p->scale > 0.f ? p->scale : 1.f / std::sqrt((float)p->head_dim);
+  g.scale_log2 = g.scale * 1.4426950408889634f;
+  return g;
+}
+
+// Which family runs problem p (assumes p validated).
+int select_impl(const na_problem* p, const na::Geom& g, const char** why) {
+  *why = "";
+  if (p->dtype == NA_F32) {
+    *why = "fp32 runs on CUDA cores (TF32 off)";
+    return NA_IMPL_SIMT;
+  }
+  if (p->impl == NA_IMPL_SIMT) return NA_IMPL_SIMT;
+  if (na::tc_supported((int)p->dtype, g, why)) return NA_IMPL_TC;
+  return NA_IMPL_SIMT;
+}
+
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+
+na_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return NA_OK;
+  return fail(NA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+na_status na_validate(const na_problem* p) {
+  na_status s = validate(p);
+  if (s == NA_OK) g_last_error.clear();
+  return s;
+}
+
+int na_selected_impl(const na_problem* p) {
+  if (validate(p) != NA_OK) return -1;
+  na::Geom g = make_geom(p);
+  const char* why;
+  return select_impl(p, g, &why);
+}
+
+na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* v, void* o,
+                 float* lse, void* stream) {
+  na_status s = validate(p);
+  if (s != NA_OK) return s;
+  if (!q || !k || !v || !o) return fail(NA_ERR_NULL, "q, k, v and o are required");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || (lse && !aligned16(lse)))
+    return fail(NA_ERR_ALIGNMENT, "tensor base pointers must be 16-byte aligned");
+  na::Geom g = make_geom(p);
+  const char* why;
+  int impl = select_impl(p, g, &why);
+  if (p->impl == NA_IMPL_TC && impl != NA_IMPL_TC)
+    return fail(NA_ERR_IMPL, "tensor-core path cannot run this problem: %s", why);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int launches = 1;
+  cudaError_t e = impl == NA_IMPL_TC ? na::tc_fwd((int)p->dtype, g, q, k, v, o, lse, st, &launches)
+                                     : na::simt_fwd((int)p->dtype, g, q, k, v, o, lse, st);
+  s = cuda_status(e, "na_fwd launch");
+  if (s == NA_OK) {
+    g_last_error.clear();
+    g_last_launches = launches;
+  }
+  return s;
+}
+
+size_t na_bwd_workspace_size(const na_problem* p) {
+  if (validate(p) != NA_OK) return 0;
+  na::Geom g = make_geom(p);
+  return (size_t)g.BH * (size_t)g.N * sizeof(float);
+}
+
+na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* v, const void* o,
+                 const void* d_o, const float* lse, void* dq, void* dk, void* dv, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  na_status s = validate(p);
+  if (s != NA_OK) return s;
+  if (!q || !k || !v || !o || !d_o || !lse || !dq || !dk || !dv)
+    return fail(NA_ERR_NULL, "q, k, v, o, d_o, lse, dq, dk, dv are required");
+  const void* ptrs[] = {q, k, v, o, d_o, lse, dq, dk, dv};
+  for (const void* ptr : ptrs)
+    if (!aligned16(ptr)) return fail(NA_ERR_ALIGNMENT, "tensor base pointers must be 16-byte aligned");
+  na::Geom g = make_geom(p);
+  const size_t need = (size_t)g.BH * (size_t)g.N * sizeof(float);
+  if (!workspace || workspace_bytes < need || !aligned16(workspace))
+    return fail(NA_ERR_WORKSPACE, "workspace needs %zu bytes (16-byte aligned), got %zu", need,
+                workspace_bytes);
+  const char* why;
+  int impl = select_impl(p, g, &why);
+  if (p->impl == NA_IMPL_TC && impl != NA_IMPL_TC)
+    return fail(NA_ERR_IMPL, "tensor-core path cannot run this problem: %s", why);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int launches = 3;
+  cudaError_t e =
+      impl == NA_IMPL_TC
+          ? na::tc_bwd((int)p->dtype, g, q, k, v, o, d_o, lse, dq, dk, dv, (float*)workspace, st,
+                       &launches)
+          : na::simt_bwd((int)p->dtype, g, q, k, v, o, d_o, lse, dq, dk, dv, (float*)workspace, st);
+  s = cuda_status(e, "na_bwd launch");
+  if (s == NA_OK) {
+    g_last_error.clear();
+    g_last_launches = launches;
+  }
+  return s;
+}
+
+const char* na_status_string(na_status s) {
+  switch (s) {
+    case NA_OK: return "ok";
+    case NA_ERR_NULL: return "null pointer";
+    case NA_ERR_RANK: return "rank not in {1,2,3}";
+    case NA_ERR_SHAPE: return "bad shape";
+    case NA_ERR_BAD_KERNEL: return "kernel_size < 1";
+    case NA_ERR_EVEN_WINDOW: return "even kernel_size on a non-causal axis";
+    case NA_ERR_BAD_DILATION: return "dilation < 1";
+    case NA_ERR_WINDOW_EXCEEDS: return "kernel_size * dilation exceeds extent";
+    case NA_ERR_DTYPE: return "unsupported dtype";
+    case NA_ERR_HEAD_DIM: return "unsupported head_dim";
+    case NA_ERR_ALIGNMENT: return "misaligned pointer";
+    case NA_ERR_LAYOUT: return "unsupported layout";
+    case NA_ERR_WORKSPACE: return "workspace too small";
+    case NA_ERR_CUDA: return "CUDA error";
+    case NA_ERR_IMPL: return "requested kernel family cannot run this problem";
+  }
+  return "unknown status";
+}
+
+const char* na_last_error(void) { return g_last_error.c_str(); }
+
+int na_last_launch_count(void) { return g_last_launches; }
+
+}  // extern "C"

@@ -1,0 +1,377 @@
+// tc_bwd.cu — fused neighborhood attention backward on sm_100a tensor cores.
+//
+// The backward is the paper's operator composition (§3.1) fused
+// FlashAttention-style, recomputing the attention weights from the saved LSE
+// instead of storing them:
+//   dP = PN(dO, V)          dS = P o (dP - D),  D_x = <dO_x, O_x>
+//   dQ = scale NN(dS, K)    dK = scale IN(dS, Q)    dV = IN(P, dO)
+// Two kernels, each output element has exactly one writer (no atomics):
+//   fna_dkdv_tc  key-stationary: a CTA owns 128 keys of one residue class and
+//                streams the query chunks of the tile's INVERSE halo
+//                [inv_start(y_lo), inv_end(y_hi)] (the IN gather pattern,
+//                P:253-258).  Per chunk: S^T = K Q^T and dP^T = V dO^T (SS MMAs),
+//                P^T = exp(scale S^T - LSE_q), dS^T = P^T (dP^T - D_q) by the
+//                compute warps (written back to TMEM as 16-bit), then
+//                dV += P^T dO and dK += dS^T Q (TS MMAs, accumulators in TMEM).
+//   fna_dq_tc    query-stationary over the forward halo: S = Q K^T, dP = dO V^T,
+//                dS = P (dP - D), dQ += dS K.
+// Warp roles (320 threads, 1 CTA per SM): warp 0 TMA producer, warp 1 TMEM
+// owner + single-thread MMA issuer, warps 2..9 compute (thread = TMEM lane =
+// stationary row; warps w and w+4 split the chunk's 128 columns in halves).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "na_geom.cuh"
+#include "na_kernels.h"
+#include "tc_common.cuh"
+#include "tc_plan.h"
+#include "tc_ptx.cuh"
+
+namespace na {
+namespace {
+
+constexpr int kStages = 2;
+constexpr int kThreads = 320;
+constexpr int kCompute = 256;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int D>
+struct BwdSmem {
+  static constexpr int kRowBytes = D * 2;
+  static constexpr int kTile = 128 * kRowBytes;
+  static constexpr int kA0 = 0;                       // stationary tile 0 (K | Q)
+  static constexpr int kA1 = kA0 + kTile;             // stationary tile 1 (V | dO)
+  static constexpr int kB0 = kA1 + kTile;             // streamed [kStages] (Q | K)
+  static constexpr int kB1 = kB0 + kStages * kTile;   // streamed [kStages] (dO | V)
+  static constexpr int kVec = kB1 + kStages * kTile;  // [2][2][128] fp32 (LSE2, D) staging
+  static constexpr int kBar = kVec + 2 * 2 * 128 * 4;
+  static constexpr int kBytes = kBar + 256;
+};
+
+// TMEM columns: [0,128) S-like accumulator, [128,256) dP-like accumulator,
+// [256, 256+D) first output, [256+D, 256+2D) second output (dK/dV kernel).
+constexpr uint32_t kColS = 0, kColP = 128, kColOut = 256;
+
+// TMEM column of the 16-bit operand for MMA k-step kk (16 partner columns):
+// each 64-column half of a chunk writes its packed values inside the columns
+// it read, so the two warps sharing a TMEM lane quarter never race.
+__device__ __forceinline__ uint32_t packed_col(int kk) { return 64 * (kk >> 2) + 8 * (kk & 3); }
+
+template <int RANK, int D, bool BF16, bool KV_STATIONARY>
+__global__ void __launch_bounds__(kThreads, 1)
+    fna_bwd_tc(const __grid_constant__ CUtensorMap map_a0, const __grid_constant__ CUtensorMap map_a1,
+               const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ CUtensorMap map_b1,
+               Geom g, TcPlan pl, const float* __restrict__ lse, const float* __restrict__ dvec,
+               void* __restrict__ out0, void* __restrict__ out1) {
+  using S = BwdSmem<D>;
+  using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  uint64_t* bar_a = bars + 0;                  // stationary tiles loaded
+  uint64_t* bar_b = bars + 1;                  // streamed stage full [kStages]
+  uint64_t* bar_e = bars + 1 + kStages;        // streamed stage empty [kStages]
+  uint64_t* bar_s = bars + 1 + 2 * kStages;    // S and dP accumulators ready
+  uint64_t* bar_p = bar_s + 1;                 // packed operands written (256 arrivals)
+  uint64_t* bar_o = bar_s + 2;                 // outputs final
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 3);
+  float* vec = reinterpret_cast<float*>(smem + S::kVec);
+
+  TileCtx<RANK> t;
+  if (!t.init(g, pl, blockIdx.x, /*inverse=*/KV_STATIONARY)) return;
+  const int nchunks = t.nchunks;
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(bar_a, 1);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(bar_b + s, 1);
+      ptx::mbar_init(bar_e + s, 1);
+    }
+    ptx::mbar_init(bar_s, 1);
+    ptx::mbar_init(bar_p, kCompute);
+    ptx::mbar_init(bar_o, 1);
+    ptx::fence_barrier_init();
+  }
+  if (pl.rows_kv < 128) {  // rows no TMA box writes must be finite (zero)
+    const int nz = (128 - pl.rows_kv) * S::kRowBytes / 16;
+    for (int i = threadIdx.x; i < 2 * kStages * nz; i += kThreads) {
+      const int buf = i / nz, off = i % nz;
+      uint4* base = reinterpret_cast<uint4*>(smem + S::kB0 + buf * S::kTile + pl.rows_kv * S::kRowBytes);
+      base[off] = make_uint4(0, 0, 0, 0);
+    }
+    ptx::fence_proxy_async();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      ptx::tma_prefetch(&map_a0);
+      ptx::tma_prefetch(&map_a1);
+      ptx::tma_prefetch(&map_b0);
+      ptx::tma_prefetch(&map_b1);
+      ptx::mbar_expect_tx(bar_a, 2 * 128 * S::kRowBytes);
+      for (int i = 0; i < pl.q_issues; ++i) {
+        t.template load_box<RANK>(&map_a0, smem + S::kA0 + i * pl.q_box_x * S::kRowBytes, bar_a,
+                                  t.q_origin, i * pl.q_box_x, g);
+        t.template load_box<RANK>(&map_a1, smem + S::kA1 + i * pl.q_box_x * S::kRowBytes, bar_a,
+                                  t.q_origin, i * pl.q_box_x, g);
+      }
+      const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes;
+      for (int j = 0; j < nchunks; ++j) {
+        const int s = j % kStages;
+        if (j >= kStages) ptx::mbar_wait(bar_e + s, ((j / kStages) - 1) & 1);
+        int org[3];
+        t.chunk_origin(pl, j, org);
+        ptx::mbar_expect_tx(bar_b + s, bytes);
+        for (int i = 0; i < pl.kv_issues; ++i) {
+          t.template load_box<RANK>(&map_b0, smem + S::kB0 + s * S::kTile + i * pl.kv_box_x * S::kRowBytes,
+                                    bar_b + s, org, i * pl.kv_box_x, g);
+          t.template load_box<RANK>(&map_b1, smem + S::kB1 + s * S::kTile + i * pl.kv_box_x * S::kRowBytes,
+                                    bar_b + s, org, i * pl.kv_box_x, g);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t kSw = D == 64 ? 2u : 4u;
+      constexpr uint32_t kSbo = 8 * S::kRowBytes;
+      const uint32_t idesc_s = ptx::make_idesc(128, pl.n_kv, BF16, false);
+      constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
+      const uint32_t a0 = ptx::smem_u32(smem + S::kA0), a1 = ptx::smem_u32(smem + S::kA1);
+      ptx::mbar_wait(bar_a, 0);
+      for (int j = 0; j < nchunks; ++j) {
+        const int s = j % kStages;
+        const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile);
+        const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile);
+        ptx::mbar_wait(bar_b + s, (j / kStages) & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
+          ptx::mma_ss(tmem + kColS, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
+                      ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), idesc_s, kk > 0);
+          ptx::mma_ss(tmem + kColP, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
+                      ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), idesc_s, kk > 0);
+        }
+        ptx::mma_commit(bar_s);
+        ptx::mbar_wait(bar_p, j & 1);
+        ptx::tc_fence_after();
+        for (int kk = 0; kk < pl.n_kv / 16; ++kk) {
+          const uint32_t pc = packed_col(kk);
+          const uint32_t boff = kk * 16 * S::kRowBytes;
+          if constexpr (KV_STATIONARY) {
+            // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
+            ptx::mma_ts(tmem + kColOut + D, tmem + kColS + pc,
+                        ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_ts(tmem + kColOut, tmem + kColP + pc,
+                        ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+          } else {
+            // dQ += dS K
+            ptx::mma_ts(tmem + kColOut, tmem + kColS + pc,
+                        ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+          }
+        }
+        ptx::mma_commit(bar_e + s);
+      }
+      ptx::mma_commit(bar_o);
+    }
+  } else {
+    // ===================== compute warps (256 threads) =====================
+    const int cw = warp - 2;             // 0..7
+    const int quarter = warp & 3;
+    const int half = cw >> 2;            // which 64 columns of a chunk
+    const int row = quarter * 32 + lane;
+    const int ctid = cw * 32 + lane;     // 0..255
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    RowCtx<RANK> r;
+    r.init(g, pl, t, row, /*inverse=*/KV_STATIONARY);
+    const float sl2 = g.scale_log2;
+    float row_lse2 = 0.f, row_d = 0.f;
+    if constexpr (!KV_STATIONARY) {
+      if (r.valid) {
+        const long long tok = r.out_offset(g, t) / g.D;
+        row_lse2 = lse[tok] * kLog2e;
+        row_d = dvec[tok];
+      }
+    }
+    for (int j = 0; j < nchunks; ++j) {
+      int org[3];
+      t.chunk_origin(pl, j, org);
+      uint32_t mw[4];
+      r.chunk_mask(pl, org, mw);
+      float* cv = vec + (j & 1) * 256;   // [LSE2 x128 | D x128] of this chunk's columns
+      if constexpr (KV_STATIONARY) {
+        // stage the partner (query) LSE and D values of this chunk's columns
+        const int col = ctid & 127, which = ctid >> 7;
+        float val = 0.f;
+        if (col < pl.rows_kv) {
+          int cc[3], rem = col;
+          bool ok = true;
+          long long tok = 0;
+#pragma unroll
+          for (int a = 2; a >= 0; --a) {
+            if (a >= RANK) continue;
+            cc[a] = org[a] + rem % pl.ckv[a];
+            rem /= pl.ckv[a];
+            ok = ok && cc[a] < t.Lr[a];
+            tok += (long long)(t.r[a] + g.dil[a] * cc[a]) * g.tstride[a];
+          }
+          if (ok) {
+            tok += (long long)t.bh * g.N;
+            val = which == 0 ? lse[tok] * kLog2e : dvec[tok];
+          }
+        }
+        cv[which * 128 + col] = val;
+        ptx::named_bar_sync(1, kCompute);
+      }
+      ptx::mbar_wait(bar_s, j & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int gq = 0; gq < 2; ++gq) {
+        const int c0 = half * 64 + gq * 32;
+        uint32_t sv[32], pv[32];
+        NA_TMEM_LD32(trow + kColS + c0, sv);
+        NA_TMEM_LD32(trow + kColP + c0, pv);
+        ptx::tmem_ld_wait();
+        const uint32_t bits = mw[c0 >> 5];
+        uint32_t pk_p[16], pk_s[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float p2[2], ds2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cc = c + e;
+            const float lse2 = KV_STATIONARY ? cv[c0 + cc] : row_lse2;
+            const float dd = KV_STATIONARY ? cv[128 + c0 + cc] : row_d;
+            const float p = (bits >> cc) & 1u ? ptx::ex2(__uint_as_float(sv[cc]) * sl2 - lse2) : 0.f;
+            p2[e] = p;
+            ds2[e] = p * (__uint_as_float(pv[cc]) - dd);
+          }
+          pk_p[c >> 1] = pack2<BF16>(p2[0], p2[1]);
+          pk_s[c >> 1] = pack2<BF16>(ds2[0], ds2[1]);
+        }
+        const uint32_t pc = 64 * half + 16 * gq;  // == packed_col(kk) for this group's kk
+        if constexpr (KV_STATIONARY) {
+          NA_TMEM_ST16(trow + kColS + pc, pk_p);
+          NA_TMEM_ST16(trow + kColP + pc, pk_s);
+        } else {
+          NA_TMEM_ST16(trow + kColS + pc, pk_s);
+        }
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(bar_p);
+    }
+    // ---- epilogue ----
+    ptx::mbar_wait(bar_o, 0);
+    ptx::tc_fence_after();
+    // KV-stationary: half 0 writes dK (x scale), half 1 writes dV.  Q-stationary:
+    // the two halves split dQ's D columns.
+    const long long off = r.out_offset(g, t);
+    constexpr int kCols = KV_STATIONARY ? D : D / 2;
+    const uint32_t src = KV_STATIONARY ? kColOut + half * D : kColOut + half * (D / 2);
+    T* dst = reinterpret_cast<T*>(KV_STATIONARY && half ? out1 : out0) + off +
+             (KV_STATIONARY ? 0 : half * (D / 2));
+    const float mul = (KV_STATIONARY && half) ? 1.f : g.scale;
+#pragma unroll
+    for (int c0 = 0; c0 < kCols; c0 += 16) {
+      uint32_t ov[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3]), "=r"(ov[4]), "=r"(ov[5]), "=r"(ov[6]),
+            "=r"(ov[7]), "=r"(ov[8]), "=r"(ov[9]), "=r"(ov[10]), "=r"(ov[11]), "=r"(ov[12]),
+            "=r"(ov[13]), "=r"(ov[14]), "=r"(ov[15])
+          : "r"(trow + src + c0));
+      ptx::tmem_ld_wait();
+      if (r.valid) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int c = 0; c < 16; c += 2)
+          pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+        d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int RANK, int D, bool BF16>
+cudaError_t launch_both(const Geom& g, const TcPlan& pl, const CUtensorMap* m, const float* lse,
+                        const float* dvec, void* dq, void* dk, void* dv, cudaStream_t st) {
+  // m: [0] Q tile, [1] K tile, [2] V tile, [3] dO tile, [4] Q chunk, [5] K chunk,
+  //    [6] V chunk, [7] dO chunk
+  const int smem = BwdSmem<D>::kBytes + 1024;
+  auto kdkdv = fna_bwd_tc<RANK, D, BF16, true>;
+  auto kdq = fna_bwd_tc<RANK, D, BF16, false>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kdkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kdq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long long grid = (long long)g.BH * pl.nres * pl.tiles;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  kdkdv<<<(unsigned)grid, kThreads, smem, st>>>(m[1], m[2], m[4], m[7], g, pl, lse, dvec, dk, dv);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  kdq<<<(unsigned)grid, kThreads, smem, st>>>(m[0], m[3], m[5], m[6], g, pl, lse, dvec, dq, nullptr);
+  return cudaGetLastError();
+}
+
+template <int RANK>
+cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const CUtensorMap* m,
+                    const float* lse, const float* dvec, void* dq, void* dk, void* dv,
+                    cudaStream_t st) {
+  const bool bf = dtype == 2;
+  if (g.D == 64)
+    return bf ? launch_both<RANK, 64, true>(g, pl, m, lse, dvec, dq, dk, dv, st)
+              : launch_both<RANK, 64, false>(g, pl, m, lse, dvec, dq, dk, dv, st);
+  return bf ? launch_both<RANK, 32, true>(g, pl, m, lse, dvec, dq, dk, dv, st)
+            : launch_both<RANK, 32, false>(g, pl, m, lse, dvec, dq, dk, dv, st);
+}
+
+}  // namespace
+
+cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+                   const void* o, const void* d_o, const float* lse, void* dq, void* dk, void* dv,
+                   float* Dvec, cudaStream_t st, int* launches) {
+  const char* why;
+  if (!tc_supported(dtype, g, &why)) return cudaErrorNotSupported;
+  cudaError_t e = bwd_preprocess(dtype, g, o, d_o, Dvec, st);
+  if (e != cudaSuccess) return e;
+  TcPlan pl = make_plan(g, 128);
+  CUtensorMap m[8];
+  const void* ptrs[4] = {q, k, v, d_o};
+  for (int i = 0; i < 4; ++i) {
+    if ((e = make_map(&m[i], dtype, g, ptrs[i], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+    if ((e = make_map(&m[4 + i], dtype, g, ptrs[i], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+  }
+  *launches = 3;
+  switch (g.rank) {
+    case 1: return by_type<1>(dtype, g, pl, m, lse, Dvec, dq, dk, dv, st);
+    case 2: return by_type<2>(dtype, g, pl, m, lse, Dvec, dq, dk, dv, st);
+    default: return by_type<3>(dtype, g, pl, m, lse, Dvec, dq, dk, dv, st);
+  }
+}
+
+}  // namespace na

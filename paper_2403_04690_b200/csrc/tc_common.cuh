@@ -1,0 +1,202 @@
+// tc_common.cuh — tile / row bookkeeping shared by the tcgen05 kernels, and
+// the host helpers that build their plan and TMA tensor maps.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <type_traits>
+
+#include "na_geom.cuh"
+#include "tc_plan.h"
+#include "tc_ptx.cuh"
+
+namespace na {
+
+// Host side (tc_host.cpp).
+TcPlan make_plan(const Geom& g, int tile_rows);
+cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base,
+                     const int box[3], int box_x);
+
+template <bool BF16>
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  if constexpr (BF16) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
+// Which (b*h, residue class, tile) a CTA owns, and the tile's halo.
+// `tile` = the 128-token box this CTA is stationary on (queries in the
+// forward and dQ kernels, keys in the dK/dV kernel); `inverse` selects
+// whether its streamed partner range is the forward halo
+// [start(lo), end(hi)] or the inverse halo [inv_start(lo), inv_end(hi)].
+template <int RANK>
+struct TileCtx {
+  int bh;
+  int r[3];       // residue per axis
+  int Lr[3];      // class size per axis
+  int q_origin[3];
+  int qv[3];      // valid extent of the tile per axis
+  int lo[3];      // halo low corner
+  int nch[3];     // chunks per axis
+  int nchunks;
+
+  __device__ __forceinline__ bool init(const Geom& g, const TcPlan& pl, unsigned block,
+                                       bool inverse = false) {
+    int tile = (int)(block % (unsigned)pl.tiles);
+    unsigned rest = block / (unsigned)pl.tiles;
+    int res = (int)(rest % (unsigned)pl.nres);
+    bh = (int)(rest / (unsigned)pl.nres);
+    nchunks = 1;
+#pragma unroll
+    for (int a = 2; a >= 0; --a) {
+      if (a >= RANK) {
+        r[a] = 0; Lr[a] = 1; q_origin[a] = 0; qv[a] = 1; lo[a] = 0; nch[a] = 1;
+        continue;
+      }
+      r[a] = res % g.dil[a];
+      res /= g.dil[a];
+      const int ti = tile % pl.ntile[a];
+      tile /= pl.ntile[a];
+      Lr[a] = class_size(g.L[a], g.dil[a], r[a]);
+      q_origin[a] = ti * pl.tq[a];
+      qv[a] = min(pl.tq[a], Lr[a] - q_origin[a]);
+      int hi;
+      if (!inverse) {
+        lo[a] = win_start(q_origin[a], Lr[a], g.k[a], g.causal[a]);
+        hi = win_end(q_origin[a] + qv[a] - 1, Lr[a], g.k[a], g.causal[a]);
+      } else {
+        lo[a] = inv_start(q_origin[a], Lr[a], g.k[a], g.causal[a]);
+        hi = inv_end(q_origin[a] + qv[a] - 1, Lr[a], g.k[a], g.causal[a]);
+      }
+      nch[a] = (hi - lo[a] + pl.ckv[a]) / pl.ckv[a];
+      nchunks *= nch[a];
+    }
+#pragma unroll
+    for (int a = 0; a < RANK; ++a)
+      if (qv[a] <= 0) return false;
+    return true;
+  }
+
+  __device__ __forceinline__ void chunk_origin(const TcPlan& pl, int j, int org[3]) const {
+    int rem = j;
+#pragma unroll
+    for (int a = 2; a >= 0; --a) {
+      if (a >= RANK) { org[a] = 0; continue; }
+      org[a] = lo[a] + (rem % nch[a]) * pl.ckv[a];
+      rem /= nch[a];
+    }
+  }
+
+  // TMA load of a box whose compacted corner is `org` (+x_off on the
+  // innermost axis).  Coordinates are original-tensor element coordinates
+  // r + dil * c; the tensor map's elementStrides = dil walks the class.
+  template <int R>
+  __device__ __forceinline__ void load_box(const CUtensorMap* m, void* dst, uint64_t* bar,
+                                           const int org[3], int x_off, const Geom& g) const {
+    if constexpr (R == 1) {
+      ptx::tma_load_3d(dst, m, bar, 0, r[0] + g.dil[0] * (org[0] + x_off), bh);
+    } else if constexpr (R == 2) {
+      ptx::tma_load_4d(dst, m, bar, 0, r[1] + g.dil[1] * (org[1] + x_off),
+                       r[0] + g.dil[0] * org[0], bh);
+    } else {
+      ptx::tma_load_5d(dst, m, bar, 0, r[2] + g.dil[2] * (org[2] + x_off),
+                       r[1] + g.dil[1] * org[1], r[0] + g.dil[0] * org[0], bh);
+    }
+  }
+};
+
+__device__ __forceinline__ void set_range(uint32_t mw[4], int lo, int hi) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    int a = lo - 32 * w, b = hi - 32 * w;
+    if (b >= 0 && a <= 31 && a <= b) {
+      a = a < 0 ? 0 : a;
+      b = b > 31 ? 31 : b;
+      mw[w] |= (0xffffffffu >> (31 - (b - a))) << a;
+    }
+  }
+}
+
+// One row (= one TMEM lane = one thread) of a stationary tile.
+template <int RANK>
+struct RowCtx {
+  int c[3];         // compacted coordinate of this row's token
+  int wlo[3], whi[3];  // partner interval per axis (window or inverse window)
+  bool valid;
+
+  __device__ __forceinline__ void init(const Geom& g, const TcPlan& pl, const TileCtx<RANK>& t,
+                                       int row, bool inverse = false) {
+    valid = true;
+    int rem = row;
+#pragma unroll
+    for (int a = 2; a >= 0; --a) {
+      if (a >= RANK) { c[a] = 0; wlo[a] = 0; whi[a] = 0; continue; }
+      const int off = rem % pl.tq[a];
+      rem /= pl.tq[a];
+      c[a] = t.q_origin[a] + off;
+      valid = valid && off < t.qv[a];
+      if (!inverse) {
+        wlo[a] = win_start(c[a], t.Lr[a], g.k[a], g.causal[a]);
+        whi[a] = win_end(c[a], t.Lr[a], g.k[a], g.causal[a]);
+      } else {
+        wlo[a] = inv_start(c[a], t.Lr[a], g.k[a], g.causal[a]);
+        whi[a] = inv_end(c[a], t.Lr[a], g.k[a], g.causal[a]);
+      }
+    }
+    if (!valid) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) { wlo[a] = 1; whi[a] = 0; }
+    }
+  }
+
+  // Element offset of this row's token in a [BH, N, D] tensor.
+  __device__ __forceinline__ long long out_offset(const Geom& g, const TileCtx<RANK>& t) const {
+    long long tok = 0;
+#pragma unroll
+    for (int a = 0; a < RANK; ++a) tok += (long long)(t.r[a] + g.dil[a] * c[a]) * g.tstride[a];
+    return ((long long)t.bh * g.N + tok) * g.D;
+  }
+
+  // Validity bitmask of the <=128 chunk columns for this row: column
+  // (lt*ckv1 + ly)*ckv2 + lx is the key at org + (lt, ly, lx).
+  __device__ __forceinline__ void chunk_mask(const TcPlan& pl, const int org[3], uint32_t mw[4]) const {
+    mw[0] = mw[1] = mw[2] = mw[3] = 0u;
+    if constexpr (RANK == 1) {
+      int lo = wlo[0] - org[0], hi = whi[0] - org[0];
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > pl.ckv[0] - 1 ? pl.ckv[0] - 1 : hi;
+      set_range(mw, lo, hi);
+    } else {
+      const int ax = RANK - 1;  // innermost axis
+      int xlo = wlo[ax] - org[ax], xhi = whi[ax] - org[ax];
+      xlo = xlo < 0 ? 0 : xlo;
+      xhi = xhi > pl.ckv[ax] - 1 ? pl.ckv[ax] - 1 : xhi;
+      if (xlo > xhi) return;
+      if constexpr (RANK == 2) {
+        for (int ly = 0; ly < pl.ckv[0]; ++ly) {
+          const int ky = org[0] + ly;
+          if (ky >= wlo[0] && ky <= whi[0]) set_range(mw, ly * pl.ckv[1] + xlo, ly * pl.ckv[1] + xhi);
+        }
+      } else {
+        for (int lt = 0; lt < pl.ckv[0]; ++lt) {
+          const int kt = org[0] + lt;
+          if (kt < wlo[0] || kt > whi[0]) continue;
+          for (int ly = 0; ly < pl.ckv[1]; ++ly) {
+            const int ky = org[1] + ly;
+            if (ky >= wlo[1] && ky <= whi[1]) {
+              const int base = (lt * pl.ckv[1] + ly) * pl.ckv[2];
+              set_range(mw, base + xlo, base + xhi);
+            }
+          }
+        }
+      }
+    }
+  }
+};
+
+}  // namespace na

@@ -1,0 +1,198 @@
+// tc_host.cpp — host side of the tcgen05 path: which problems it covers, the
+// tile planner (space-aware tiling, P:276-281 / Fig. 3) and TMA tensor maps
+// (hardware predication replaces the paper's software GETT predication,
+// P:392-402).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <mutex>
+
+#include "na_geom.cuh"
+#include "na_kernels.h"
+#include "tc_plan.h"
+
+namespace na {
+
+bool tc_supported(int dtype, const Geom& g, const char** why) {
+  if (dtype != 1 && dtype != 2) { *why = "tensor-core path is fp16/bf16 only"; return false; }
+  if (g.D != 32 && g.D != 64) { *why = "tensor-core path needs head_dim 32 or 64"; return false; }
+  for (int a = 0; a < g.rank; ++a) {
+    if (g.dil[a] > 8) { *why = "TMA element strides limit dilation to <= 8"; return false; }
+  }
+  if (g.rank >= 2) {
+    // every non-innermost tile/box extent must satisfy extent * dilation <= 256
+    for (int a = 0; a < g.rank; ++a)
+      if (g.dil[a] * 1 > 256) { *why = "dilation too large"; return false; }
+  }
+  *why = "";
+  return true;
+}
+
+namespace {
+
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+int round16(int a) { return (a + 15) / 16 * 16; }
+
+// Largest power of two <= 128 with box * dil <= 256.
+int box_x_for(int ext, int dil) {
+  int b = ext;
+  while (b * dil > 256) b /= 2;
+  return b;
+}
+
+}  // namespace
+
+TcPlan make_plan(const Geom& g, int tile_rows) {
+  TcPlan pl{};
+  int Lmax[3];
+  for (int a = 0; a < 3; ++a) {
+    Lmax[a] = a < g.rank ? ceil_div(g.L[a], g.dil[a]) : 1;
+    pl.tq[a] = pl.ckv[a] = 1;
+  }
+  pl.nres = 1;
+  for (int a = 0; a < g.rank; ++a) pl.nres *= g.dil[a];
+  if (g.rank == 1) {
+    pl.tq[0] = tile_rows;
+    pl.ckv[0] = 128;
+    pl.q_box_x = box_x_for(tile_rows, g.dil[0]);
+    pl.kv_box_x = box_x_for(128, g.dil[0]);
+  } else {
+    // Enumerate power-of-two tiles (product tile_rows) and KV boxes covering the
+    // interior halo t + k - 1; minimise MMA columns (+ per-chunk overhead) per
+    // useful query row.
+    const int R = g.rank;
+    double best = 1e30;
+    int t[3] = {1, 1, 1};
+    auto consider = [&](const int tq[3]) {
+      int h[3], valid_rows = 1;
+      for (int a = 0; a < R; ++a) {
+        if (tq[a] * g.dil[a] > 256) return;
+        h[a] = std::min(tq[a] + g.k[a] - 1, Lmax[a]);
+        valid_rows *= std::min(tq[a], Lmax[a]);
+      }
+      const int ax = R - 1;
+      // candidate innermost box widths
+      for (int split = 1; split <= 4; ++split) {
+        int cx = ceil_div(h[ax], split);
+        if (cx > 128 || cx * g.dil[ax] > 256) continue;
+        int ck[3] = {1, 1, 1};
+        ck[ax] = cx;
+        int room = 128 / cx;
+        // fill remaining axes from inner to outer, balancing chunk counts
+        for (int a = ax - 1; a >= 0; --a) {
+          int c = std::min(h[a], room);
+          if (c < 1) c = 1;
+          int n = ceil_div(h[a], c);
+          c = ceil_div(h[a], n);  // balance
+          while (c * g.dil[a] > 256) c--;
+          ck[a] = c;
+          room = std::max(1, room / c);
+        }
+        int rows = 1, chunks = 1;
+        for (int a = 0; a < R; ++a) {
+          rows *= ck[a];
+          chunks *= ceil_div(h[a], ck[a]);
+        }
+        if (rows > 128) continue;
+        const double cost = (double)chunks * (round16(rows) + 48) / valid_rows;
+        if (cost < best) {
+          best = cost;
+          for (int a = 0; a < 3; ++a) {
+            pl.tq[a] = a < R ? tq[a] : 1;
+            pl.ckv[a] = a < R ? ck[a] : 1;
+          }
+        }
+      }
+    };
+    if (R == 2) {
+      for (int tx = 1; tx <= tile_rows; tx *= 2) {
+        t[1] = tx;
+        t[0] = tile_rows / tx;
+        consider(t);
+      }
+    } else {
+      for (int tx = 1; tx <= tile_rows; tx *= 2)
+        for (int ty = 1; tx * ty <= tile_rows; ty *= 2) {
+          t[2] = tx;
+          t[1] = ty;
+          t[0] = tile_rows / (tx * ty);
+          consider(t);
+        }
+    }
+    pl.q_box_x = pl.tq[R - 1];
+    pl.kv_box_x = pl.ckv[R - 1];
+  }
+  pl.q_issues = pl.tq[g.rank - 1] / pl.q_box_x;
+  pl.kv_issues = pl.ckv[g.rank - 1] / pl.kv_box_x;
+  pl.tiles = 1;
+  pl.rows_kv = 1;
+  for (int a = 0; a < 3; ++a) {
+    pl.ntile[a] = a < g.rank ? ceil_div(Lmax[a], pl.tq[a]) : 1;
+    pl.tiles *= pl.ntile[a];
+    pl.rows_kv *= pl.ckv[a];
+  }
+  pl.n_kv = round16(pl.rows_kv);
+  return pl;
+}
+
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+// Tensor map over a contiguous [BH, X0 (, X1 (, X2)), D] 16-bit tensor.
+// dims (innermost first) = D, X_{R-1}, ..., X_0, BH.  The box is `box`
+// compacted tokens per axis (box_x on the innermost axis, per TMA issue),
+// walked with elementStrides = dilation so one box covers one residue class.
+cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base, const int box[3],
+                     int box_x) {
+  EncodeTiled enc = encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const int R = g.rank;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t boxd[5], estr[5];
+  const cuuint64_t row = (cuuint64_t)g.D * 2;
+  dims[0] = g.D;
+  boxd[0] = g.D;
+  estr[0] = 1;
+  for (int i = 1; i <= R; ++i) {
+    const int a = R - i;
+    dims[i] = g.L[a];
+    strides[i - 1] = row * g.tstride[a];
+    const int b = (i == 1) ? box_x : box[a];
+    boxd[i] = (cuuint32_t)(b * g.dil[a]);
+    estr[i] = g.dil[a];
+  }
+  dims[R + 1] = g.BH;
+  strides[R] = row * g.N;
+  boxd[R + 1] = 1;
+  estr[R + 1] = 1;
+  const CUtensorMapSwizzle sw = g.D == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  CUresult r = enc(map, dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   R + 2, const_cast<void*>(base), dims, strides, boxd, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+}  // namespace na

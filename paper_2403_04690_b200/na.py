@@ -1,0 +1,176 @@
+"""ctypes binding of include/na.h — argument marshalling only.
+
+Every step of the computation runs in libna.so's CUDA kernels.  Tensors are
+torch CUDA tensors in the ABI layout [B, H, X0 (, X1 (, X2)), D]; the call is
+enqueued on torch's current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libna.so")
+
+NA_F32, NA_F16, NA_BF16 = 0, 1, 2
+NA_IMPL_AUTO, NA_IMPL_SIMT, NA_IMPL_TC = 0, 1, 2
+_DTYPES = {torch.float32: NA_F32, torch.float16: NA_F16, torch.bfloat16: NA_BF16}
+_IMPLS = {"auto": NA_IMPL_AUTO, "simt": NA_IMPL_SIMT, "tc": NA_IMPL_TC}
+
+
+class Problem(ctypes.Structure):
+    """Mirror of ``na_problem`` (include/na.h)."""
+    _fields_ = [
+        ("rank", ctypes.c_int32),
+        ("batch", ctypes.c_int32),
+        ("heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("extent", ctypes.c_int32 * 3),
+        ("kernel_size", ctypes.c_int32 * 3),
+        ("dilation", ctypes.c_int32 * 3),
+        ("is_causal", ctypes.c_int32 * 3),
+        ("scale", ctypes.c_float),
+        ("dtype", ctypes.c_int32),
+        ("impl", ctypes.c_int32),
+        ("strides", ctypes.c_void_p),
+    ]
+
+
+class NAError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{status_string(status)} ({status}): {detail}")
+        self.status = status
+
+
+_lib = None
+
+EXPORTS = ("na_validate", "na_fwd", "na_bwd", "na_bwd_workspace_size", "na_selected_impl",
+           "na_status_string", "na_last_error", "na_last_launch_count")
+
+
+def lib():
+    """Load libna.so (must have been built in-tree; raises if missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() or "
+                              "python -m paper_2403_04690_b200.build (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER(Problem)
+        vp = ctypes.c_void_p
+        L.na_validate.argtypes = [P]
+        L.na_validate.restype = ctypes.c_int
+        L.na_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp]
+        L.na_fwd.restype = ctypes.c_int
+        L.na_bwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
+        L.na_bwd.restype = ctypes.c_int
+        L.na_bwd_workspace_size.argtypes = [P]
+        L.na_bwd_workspace_size.restype = ctypes.c_size_t
+        L.na_selected_impl.argtypes = [P]
+        L.na_selected_impl.restype = ctypes.c_int
+        L.na_status_string.argtypes = [ctypes.c_int]
+        L.na_status_string.restype = ctypes.c_char_p
+        L.na_last_error.argtypes = []
+        L.na_last_error.restype = ctypes.c_char_p
+        L.na_last_launch_count.argtypes = []
+        L.na_last_launch_count.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def status_string(s: int) -> str:
+    return lib().na_status_string(s).decode()
+
+
+def _check(status: int):
+    if status != 0:
+        raise NAError(status, lib().na_last_error().decode())
+
+
+def make_problem(batch, heads, extent, head_dim, kernel_size, dilation=None, is_causal=None,
+                 scale=None, dtype=torch.float16, impl="auto") -> Problem:
+    r = len(extent)
+    if isinstance(kernel_size, int):
+        kernel_size = [kernel_size] * r
+    dilation = [dilation] * r if isinstance(dilation, int) else (dilation or [1] * r)
+    is_causal = [is_causal] * r if isinstance(is_causal, bool) else (is_causal or [False] * r)
+    pad = lambda xs, f: [int(x) for x in xs] + [f] * (3 - len(xs))
+    A = ctypes.c_int32 * 3
+    return Problem(r, batch, heads, head_dim, A(*pad(extent, 1)), A(*pad(kernel_size, 1)),
+                   A(*pad(dilation, 1)), A(*pad([bool(c) for c in is_causal], 0)),
+                   float(scale) if scale else 0.0, _DTYPES[dtype], _IMPLS[impl], None)
+
+
+def _problem_from(q: torch.Tensor, kernel_size, dilation, is_causal, scale, impl) -> Problem:
+    if q.dim() < 4 or q.dim() > 6:
+        raise ValueError("expected [B, H, X0 (, X1 (, X2)), D]")
+    B, H, *ext, D = q.shape
+    return make_problem(B, H, ext, D, kernel_size, dilation, is_causal, scale, q.dtype, impl)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _need(t: torch.Tensor, like: torch.Tensor, name: str):
+    if t.device != like.device or t.dtype != like.dtype or t.shape != like.shape or \
+            not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {like.dtype} tensor of shape "
+                         f"{tuple(like.shape)} on {like.device}")
+
+
+def na_validate(p: Problem) -> int:
+    return lib().na_validate(ctypes.byref(p))
+
+
+def na_selected_impl(p: Problem) -> int:
+    return lib().na_selected_impl(ctypes.byref(p))
+
+
+def na_bwd_workspace_size(p: Problem) -> int:
+    return lib().na_bwd_workspace_size(ctypes.byref(p))
+
+
+def last_launch_count() -> int:
+    return lib().na_last_launch_count()
+
+
+def na_fwd(q, k, v, kernel_size, dilation=None, is_causal=None, scale=None, impl="auto",
+           out=None, lse=None, return_lse=True):
+    """Fused NA forward.  Returns (O, LSE) (LSE fp32 [B,H,X...]) or O."""
+    p = _problem_from(q, kernel_size, dilation, is_causal, scale, impl)
+    for t, n in ((q, "q"), (k, "k"), (v, "v")):
+        _need(t, q, n)
+    o = torch.empty_like(q) if out is None else out
+    _need(o, q, "out")
+    if return_lse and lse is None:
+        lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
+    _check(lib().na_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                        _ptr(lse) if return_lse else None, _stream()))
+    return (o, lse) if return_lse else o
+
+
+def na_bwd(q, k, v, o, d_o, lse, kernel_size, dilation=None, is_causal=None, scale=None,
+           impl="auto", dq=None, dk=None, dv=None, workspace=None):
+    """Fused NA backward.  Returns (dQ, dK, dV)."""
+    p = _problem_from(q, kernel_size, dilation, is_causal, scale, impl)
+    for t, n in ((k, "k"), (v, "v"), (o, "o"), (d_o, "d_o")):
+        _need(t, q, n)
+    if lse.dtype != torch.float32 or lse.shape != q.shape[:-1] or not lse.is_contiguous():
+        raise ValueError("lse must be a contiguous fp32 [B, H, X...] tensor")
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(q) if dk is None else dk
+    dv = torch.empty_like(q) if dv is None else dv
+    need = na_bwd_workspace_size(p)
+    if workspace is None:
+        workspace = torch.empty((max(need, 16) + 3) // 4, dtype=torch.float32, device=q.device)
+    _check(lib().na_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(d_o), _ptr(lse),
+                        _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace),
+                        workspace.numel() * workspace.element_size(), _stream()))
+    return dq, dk, dv

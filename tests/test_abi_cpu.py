@@ -1,0 +1,118 @@
+"""Host-side checks of the C ABI (no GPU needed): the library loads, exports
+every entry point include/na.h declares, and validates problems exactly as
+documented (SPEC S:62-70 constraint list, readings R2/R6)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+import torch
+
+from paper_2403_04690_b200 import build as na_build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def na():
+    na_build.build()
+    import paper_2403_04690_b200 as pkg
+    pkg.lib()
+    return pkg
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "na.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(na_[a-z_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol(na):
+    names = header_functions()
+    assert {"na_fwd", "na_bwd", "na_validate", "na_bwd_workspace_size"} <= set(names)
+    out = subprocess.run(["nm", "-D", "--defined-only", na.na.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (na_[a-z_]+)\b", out))
+    assert set(names) <= exported, set(names) - exported
+    L = na.lib()
+    for n in names:
+        assert hasattr(L, n)
+
+
+def test_library_is_sm100a(na):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", na.na.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def P(na, **kw):
+    base = dict(batch=1, heads=1, extent=[16], head_dim=64, kernel_size=[3])
+    base.update(kw)
+    return na.make_problem(**base)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(), 0),
+    (dict(extent=[5], kernel_size=[3]), 0),
+    (dict(extent=[5], kernel_size=[4]), 5),                     # S:69 even window
+    (dict(extent=[8], kernel_size=[5], dilation=[2]), 7),       # S:70 exceeds class
+    (dict(extent=[8], kernel_size=[4], is_causal=[True]), 0),   # even k ok when causal
+    (dict(extent=[8], kernel_size=[3], dilation=[0]), 6),
+    (dict(extent=[8], kernel_size=[0]), 4),
+    (dict(head_dim=12), 9),
+    (dict(head_dim=264), 9),
+    (dict(head_dim=12, dtype=torch.float32), 0),
+    (dict(extent=[4, 4, 4, 4], kernel_size=[3, 3, 3, 3]), 2),
+    (dict(batch=0), 3),
+    (dict(extent=[0], kernel_size=[1]), 3),
+    (dict(extent=[9, 9], kernel_size=[3, 9], dilation=[1, 2]), 7),
+])
+def test_validation_codes(na, kw, status):
+    if len(kw.get("extent", [1])) > 3:
+        p = P(na)
+        p.rank = 4
+    else:
+        p = P(na, **kw)
+    assert na.na_validate(p) == status
+    if status:
+        assert na.lib().na_last_error().decode()
+
+
+def test_layout_and_impl_codes(na):
+    p = P(na)
+    arr = (ctypes.c_int64 * 6)(*range(6))
+    p.strides = ctypes.cast(arr, ctypes.c_void_p)
+    assert na.na_validate(p) == 11
+    p = P(na)
+    p.impl = 7
+    assert na.na_validate(p) == 14
+
+
+def test_workspace_size(na):
+    p = P(na, batch=2, heads=3, extent=[7, 5], kernel_size=[3, 3])
+    assert na.na_bwd_workspace_size(p) == 2 * 3 * 35 * 4
+    assert na.na_bwd_workspace_size(P(na, kernel_size=[4])) == 0
+
+
+def test_fp32_selects_simt(na):
+    assert na.na_selected_impl(P(na, dtype=torch.float32)) == na.NA_IMPL_SIMT
+    assert na.na_selected_impl(P(na, kernel_size=[4])) == -1
+
+
+def test_fwd_rejects_before_launch(na):
+    """Validation errors are returned synchronously with no launch (no GPU here)."""
+    L = na.lib()
+    p = P(na, kernel_size=[4])
+    assert L.na_fwd(ctypes.byref(p), None, None, None, None, None, None) == 5
+    p = P(na)
+    assert L.na_fwd(ctypes.byref(p), None, None, None, None, None, None) == 1
+    fake = ctypes.c_void_p(0x1008)
+    assert L.na_fwd(ctypes.byref(p), fake, fake, fake, fake, None, None) == 10
+    ok = ctypes.c_void_p(0x1000)
+    assert L.na_bwd(ctypes.byref(p), ok, ok, ok, ok, ok, ok, ok, ok, ok, None, 0, None) == 12
+
+
+def test_status_strings(na):
+    for s in range(15):
+        assert na.status_string(s)

@@ -1,0 +1,191 @@
+"""GPU parity: libna.so (through its C ABI) vs the fp64 CPU oracle.
+
+Tolerances (north_star, R14): max-abs <= 1e-4 for fp32 inputs
+(CUDA cores, TF32 off) and <= 1e-2 on O/dQ/dK/dV for fp16/bf16 with
+unit-normal inputs; LSE <= 1e-4 (fp32) / 2e-3 (16-bit).  The oracle consumes
+the same rounded inputs the GPU sees.
+"""
+import itertools
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import na_synth
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.float16: 1e-2, torch.bfloat16: 1e-2}
+LSE_TOL = {torch.float32: 1e-4, torch.float16: 2e-3, torch.bfloat16: 2e-3}
+
+
+@pytest.fixture(scope="module")
+def na():
+    import paper_2403_04690_b200 as pkg
+    pkg.lib()
+    return pkg
+
+
+def oracle_problem(cfg, scale=0.0):
+    return oracle.make_problem(cfg.batch, cfg.heads, list(cfg.extent), cfg.head_dim,
+                               list(cfg.kernel_size), list(cfg.dilation),
+                               [int(c) for c in cfg.is_causal], scale)
+
+
+def run_gpu(na, cfg, q, k, v, do, impl):
+    kw = dict(kernel_size=list(cfg.kernel_size), dilation=list(cfg.dilation),
+              is_causal=[bool(c) for c in cfg.is_causal], impl=impl)
+    qd, kd, vd, dod = (t.cuda() for t in (q, k, v, do))
+    o, lse = na.na_fwd(qd, kd, vd, **kw)
+    dq, dk, dv = na.na_bwd(qd, kd, vd, o, dod, lse, **kw)
+    torch.cuda.synchronize()
+    return [t.float().cpu() for t in (o, lse, dq, dk, dv)]
+
+
+def max_err(a, b):
+    return float(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64)).max())
+
+
+# unit roundoff of the output dtype: the final fp32 -> dtype conversion alone
+# may move a value by half an ulp (R14)
+HALF_ULP_BITS = {torch.float32: 24, torch.float16: 11, torch.bfloat16: 8}
+
+
+def excess(gpu, ref, dt):
+    """max over elements of |gpu - ref| - (tol + half-ulp_dtype(|ref|)); <= 0 passes."""
+    g = np.asarray(gpu, np.float64)
+    r = np.asarray(ref, np.float64)
+    mag = np.maximum(np.abs(r), 2.0 ** -14)
+    half_ulp = 2.0 ** (np.floor(np.log2(mag)) - HALF_ULP_BITS[dt])
+    return float((np.abs(g - r) - (TOL[dt] + half_ulp)).max())
+
+
+SMALL = [
+    # extent, kernel, dilation, causal
+    ([300], [7], [1], [0]),
+    ([300], [1], [1], [0]),
+    ([300], [33], [3], [0]),
+    ([300], [255], [1], [0]),
+    ([300], [64], [2], [1]),
+    ([257], [31], [4], [1]),
+    ([37, 20], [7, 5], [1, 2], [0, 0]),
+    ([23, 41], [3, 9], [2, 1], [1, 0]),
+    ([6, 10, 13], [3, 5, 7], [1, 1, 1], [1, 0, 0]),
+    ([8, 9, 12], [3, 3, 3], [2, 1, 2], [0, 1, 0]),
+]
+
+
+def small_cases():
+    for (ext, ker, dil, cau), D, dt in itertools.product(SMALL, [32, 64],
+                                                          [torch.float16, torch.bfloat16]):
+        yield pytest.param(ext, ker, dil, cau, D, dt, id=f"{ext}-k{ker}-d{dil}-c{cau}-D{D}-{str(dt)[6:]}")
+    for ext, ker, dil, cau in SMALL[::3]:
+        yield pytest.param(ext, ker, dil, cau, 16, torch.float32, id=f"{ext}-k{ker}-fp32")
+
+
+@pytest.mark.parametrize("ext,ker,dil,cau,D,dt", list(small_cases()))
+@pytest.mark.parametrize("impl", ["simt", "tc"])
+def test_small_sweep_matches_oracle(na, impl, ext, ker, dil, cau, D, dt):
+    cfg = na_synth.small_config(ext, ker, dil, cau, head_dim=D, batch=1, heads=2, dtype=dt)
+    p = na.make_problem(cfg.batch, cfg.heads, list(ext), D, ker, dil, [bool(c) for c in cau],
+                        dtype=dt, impl=impl)
+    if impl == "tc" and na.na_selected_impl(p) != na.NA_IMPL_TC:
+        pytest.skip("problem outside the tensor-core path")
+    q, k, v, do = na_synth.make_inputs(cfg, salt=7)
+    o, lse, dq, dk, dv = run_gpu(na, cfg, q, k, v, do, impl)
+    op = oracle_problem(cfg)
+    ro, rlse = oracle.fwd(op, q, k, v)
+    rdq, rdk, rdv = oracle.bwd(op, q, k, v, do)
+    N = cfg.tokens
+    shp = (cfg.batch, cfg.heads, N, D)
+    assert excess(o.reshape(shp), ro, dt) <= 0, max_err(o.reshape(shp), ro)
+    assert max_err(lse.reshape(shp[:-1]), rlse) <= LSE_TOL[dt]
+    assert excess(dq.reshape(shp), rdq, dt) <= 0, max_err(dq.reshape(shp), rdq)
+    assert excess(dk.reshape(shp), rdk, dt) <= 0, max_err(dk.reshape(shp), rdk)
+    assert excess(dv.reshape(shp), rdv, dt) <= 0, max_err(dv.reshape(shp), rdv)
+
+
+@pytest.mark.parametrize("impl", ["simt", "tc"])
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+def test_kernel_one_is_exact(na, impl, dt):
+    """kernel size 1 -> O == V bitwise, dV == dO bitwise, dQ = dK = 0.
+    dQ/dK are P (dP - D) with P = 1: zero up to the rounding difference of two
+    fp32 dot products summed in different orders (D_x by the preprocess
+    kernel, dP by the tensor core), hence |dQ|, |dK| <= 1e-5."""
+    cfg = na_synth.small_config([9, 20], [1, 1], [1, 2], [0, 0], head_dim=64, dtype=dt)
+    p = na.make_problem(1, 2, [9, 20], 64, [1, 1], [1, 2], dtype=dt, impl=impl)
+    if impl == "tc" and na.na_selected_impl(p) != na.NA_IMPL_TC:
+        pytest.skip("problem outside the tensor-core path")
+    q, k, v, do = na_synth.make_inputs(cfg, device="cuda", salt=3)
+    o, lse = na.na_fwd(q, k, v, [1, 1], [1, 2], impl=impl)
+    dq, dk, dv = na.na_bwd(q, k, v, o, do, lse, [1, 1], [1, 2], impl=impl)
+    assert torch.equal(o, v)
+    assert torch.equal(dv, do)
+    assert dq.abs().max() <= 1e-5 and dk.abs().max() <= 1e-5
+
+
+@pytest.mark.parametrize("impl", ["simt", "tc"])
+def test_no_nan_with_masked_chunks(na, impl):
+    """Dilation + causal leave whole KV chunks masked for some rows (R11)."""
+    cfg = na_synth.small_config([517], [5], [8], [1], head_dim=64, dtype=torch.float16)
+    q, k, v, do = (t.cuda() for t in na_synth.make_inputs(cfg, salt=11))
+    kw = dict(kernel_size=[5], dilation=[8], is_causal=[True], impl=impl)
+    try:
+        o, lse = na.na_fwd(q, k, v, **kw)
+    except na.NAError:
+        pytest.skip("problem outside the tensor-core path")
+    dq, dk, dv = na.na_bwd(q, k, v, o, do, lse, **kw)
+    for t in (o, lse, dq, dk, dv):
+        assert torch.isfinite(t).all()
+
+
+def test_deterministic(na):
+    cfg = na_synth.small_config([40, 24], [7, 7], [2, 1], [0, 1], head_dim=64, dtype=torch.bfloat16)
+    q, k, v, do = (t.cuda() for t in na_synth.make_inputs(cfg, salt=5))
+    kw = dict(kernel_size=[7, 7], dilation=[2, 1], is_causal=[False, True])
+    r1 = [na.na_fwd(q, k, v, **kw)[0]]
+    r1 += list(na.na_bwd(q, k, v, r1[0], do, na.na_fwd(q, k, v, **kw)[1], **kw))
+    r2 = [na.na_fwd(q, k, v, **kw)[0]]
+    r2 += list(na.na_bwd(q, k, v, r2[0], do, na.na_fwd(q, k, v, **kw)[1], **kw))
+    for a, b in zip(r1, r2):
+        assert torch.equal(a, b)
+
+
+# ------------------------------------------------------- BASELINE configs
+
+CONFIG_NAMES = ["A", "B_d1", "B_d1_causal", "B_d4", "B_d4_causal", "C_d1", "C_d8", "D_d2", "E"]
+
+
+@pytest.mark.parametrize("name", CONFIG_NAMES)
+def test_baseline_config_sampled(na, name):
+    """Full BASELINE.json sizes in the launch configuration bench.py times
+    (impl=auto); outputs compared with the oracle at sampled tokens."""
+    cfg = na_synth.CONFIGS[name]
+    q, k, v, do = na_synth.make_inputs(cfg, device="cuda")
+    kw = dict(kernel_size=list(cfg.kernel_size), dilation=list(cfg.dilation),
+              is_causal=[bool(c) for c in cfg.is_causal])
+    o, lse = na.na_fwd(q, k, v, **kw)
+    dq, dk, dv = na.na_bwd(q, k, v, o, do, lse, **kw)
+    torch.cuda.synchronize()
+    BH, N, D = cfg.batch * cfg.heads, cfg.tokens, cfg.head_dim
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    n_f, n_b = (BH * N, BH * N) if name == "A" else (64, 12)
+    toks = np.sort(rng.choice(BH * N, size=n_f, replace=False))
+    # always include the first and last token of some slice (borders)
+    toks[0], toks[-1] = 0, BH * N - 1
+    hq, hk, hv, hdo = (t.cpu() for t in (q, k, v, do))
+    op = oracle_problem(cfg)
+    ro, rlse = oracle.fwd_tokens(op, hq, hk, hv, toks)
+    dt = cfg.dtype
+    flat = lambda t: t.reshape(BH * N, -1)
+    assert excess(flat(o)[toks].float().cpu(), ro, dt) <= 0
+    assert max_err(lse.reshape(-1)[toks].cpu(), rlse) <= LSE_TOL[dt]
+    bt = toks if name == "A" else np.sort(rng.choice(BH * N, size=n_b, replace=False))
+    rdq, rdk, rdv = oracle.bwd_tokens(op, hq, hk, hv, hdo, bt)
+    assert excess(flat(dq)[bt].float().cpu(), rdq, dt) <= 0
+    assert excess(flat(dk)[bt].float().cpu(), rdk, dt) <= 0
+    assert excess(flat(dv)[bt].float().cpu(), rdv, dt) <= 0
+    for t in (o, lse, dq, dk, dv):
+        assert torch.isfinite(t).all()
