@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Benchmark of the fused neighborhood attention hot path (libna.so) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+Workload (BASELINE.json configs[1], the one the metric is quoted on that fits
+one GPU): 1-D NA, fp16, B=8 H=16 L=16384 D=64, kernel 255, dilation {1,4} x
+{non-causal, causal}.  One STEP = na_fwd + na_bwd of all four variants on one
+batch (every §8(a) row of SURVEY.md).  Inputs are unit-normal, seeded per
+(b, h) (na_synth), resident in HBM before timing.
+
+metric/unit: BASELINE.json's metric; `value` = effective TFLOP/s of the whole
+step over all ranks, with the paper's nominal FLOP count 4*N*l*D per (b,h)
+forward and 10*N*l*D backward (2.5x, FlashAttention convention);
+l = 255.  Multi-GPU (torchrun): each rank owns its own contiguous range of
+B*H slices (weak scaling, no collective on the data path); NCCL only gathers
+timings.  Device time = CUDA events on the launch stream, max over ranks.
+
+`--impl reference`: the arm the driver compares against is the fp64 CPU
+oracle (oracle/, test infrastructure) timed on this host's cores on a
+bounded sample of the same workload (tier rules).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import na_synth  # noqa: E402
+
+METRIC = "fused NA fwd & fwd+bwd ms, TFLOP/s vs B200 tensor peak at 1/2/4/8 GPUs"
+WORKLOAD = "1-D NA fp16 B=8 H=16 L=16384 D=64 kernel=255 dilation={1,4} x {non-causal,causal}, fwd+bwd"
+VARIANTS = ["B_d1", "B_d4", "B_d1_causal", "B_d4_causal"]
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def flops(cfg, fwd=True, bwd=True):
+    """Nominal FLOPs for the whole batch (4 b h n l d forward)."""
+    per = 4.0 * cfg.batch * cfg.heads * cfg.tokens * cfg.window * cfg.head_dim
+    return (per if fwd else 0.0) + (2.5 * per if bwd else 0.0)
+
+
+def algorithmic_bytes(cfg, kernel):
+    """Bytes a kernel must move at minimum: every
+    tensor it reads or writes once.  E = elements of one [B,H,N,D] tensor."""
+    E = cfg.batch * cfg.heads * cfg.tokens * cfg.head_dim
+    rows = cfg.batch * cfg.heads * cfg.tokens
+    s = 2 if cfg.dtype in (torch.float16, torch.bfloat16) else 4
+    return {
+        "fna_fwd_tc": 4 * E * s + 4 * rows,            # Q,K,V read; O write; LSE write
+        "fna_fwd_simt": 4 * E * s + 4 * rows,
+        "fna_bwd_pre": 2 * E * s + 4 * rows,           # O, dO read; D write
+        "fna_dkdv_tc": 6 * E * s + 8 * rows,           # Q,K,V,dO read; dK,dV write; LSE,D read
+        "fna_dkdv_simt": 6 * E * s + 8 * rows,
+        "fna_dq_tc": 5 * E * s + 8 * rows,             # Q,K,V,dO read; dQ write; LSE,D read
+        "fna_dq_simt": 5 * E * s + 8 * rows,
+    }[kernel]
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return p, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during timing."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = []
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        sm = [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in rows),
+                "samples": len(rows), "reasons": reasons}
+
+
+def init_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def reduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ native arm
+
+class Runner:
+    """Buffers and the step function for one rank's batch of the workload."""
+
+    def __init__(self, rank: int):
+        import paper_2403_04690_b200 as na
+        self.na = na
+        self.cfgs = [na_synth.CONFIGS[v] for v in VARIANTS]
+        c = self.cfgs[0]
+        bh = c.batch * c.heads
+        rng = (rank * bh, (rank + 1) * bh)  # weak scaling: this rank's own B*H slices
+        q, k, v, do = na_synth.make_inputs(c, device="cuda", bh_range=rng)
+        shape = c.shape()
+        self.q, self.k, self.v, self.do = (t.view(shape) for t in (q, k, v, do))
+        self.outs = []
+        for cfg in self.cfgs:
+            o = torch.empty(shape, dtype=c.dtype, device="cuda")
+            lse = torch.empty(shape[:-1], dtype=torch.float32, device="cuda")
+            grads = [torch.empty(shape, dtype=c.dtype, device="cuda") for _ in range(3)]
+            ws = torch.empty(c.batch * c.heads * c.tokens, dtype=torch.float32, device="cuda")
+            self.outs.append((o, lse, grads, ws))
+        self.launches = 0
+
+    def kw(self, cfg):
+        return dict(kernel_size=list(cfg.kernel_size), dilation=list(cfg.dilation),
+                    is_causal=[bool(x) for x in cfg.is_causal])
+
+    def step(self, q=None, k=None, v=None, do=None):
+        na = self.na
+        q = self.q if q is None else q
+        k = self.k if k is None else k
+        v = self.v if v is None else v
+        do = self.do if do is None else do
+        n = 0
+        for cfg, (o, lse, (dq, dk, dv), ws) in zip(self.cfgs, self.outs):
+            kw = self.kw(cfg)
+            na.na_fwd(q, k, v, out=o, lse=lse, **kw)
+            n += na.last_launch_count()
+            na.na_bwd(q, k, v, o, do, lse, dq=dq, dk=dk, dv=dv, workspace=ws, **kw)
+            n += na.last_launch_count()
+        self.launches = n
+        return n
+
+    def fwd_only(self):
+        for cfg, (o, lse, _, _) in zip(self.cfgs, self.outs):
+            self.na.na_fwd(self.q, self.k, self.v, out=o, lse=lse, **self.kw(cfg))
+
+
+def timed_steps(fn, steps, flush=None):
+    """Per-step CUDA-event device time (ms) on the current stream; the L2
+    flush between steps is outside the event pair."""
+    st = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for a, b in evs:
+        if flush is not None:
+            flush.zero_()
+        a.record(st)
+        fn()
+        b.record(st)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def oracle_sample(tokens: int, n_slices: int):
+    """Inputs + step function for the fp64 oracle on a bounded sample of the
+    workload: n_slices (b,h) slices of the B_d1 variant (k=255, D=64) cut to
+    their first `tokens` tokens, fwd (nar_fwd) + bwd (nar_bwd)."""
+    import oracle
+    base = na_synth.CONFIGS["B_d1"]
+    cfg = na_synth.small_config([tokens], list(base.kernel_size), list(base.dilation),
+                                list(base.is_causal), head_dim=base.head_dim, batch=1,
+                                heads=n_slices, dtype=base.dtype)
+    q, k, v, do = na_synth.make_inputs(cfg)
+    p = oracle.make_problem(1, n_slices, [tokens], cfg.head_dim, list(cfg.kernel_size),
+                            list(cfg.dilation), [int(c) for c in cfg.is_causal])
+
+    def step():
+        oracle.fwd(p, q, k, v)
+        oracle.bwd(p, q, k, v, do)
+
+    fl = 14.0 * n_slices * tokens * cfg.window * cfg.head_dim
+    desc = (f"{n_slices} (b,h) slices x first {tokens} tokens of B_d1 (k=255, D=64, fp16 "
+            f"inputs upcast), fwd+bwd in fp64")
+    return step, fl, desc
+
+
+def cpu_baseline_sample():
+    import oracle
+    cores = oracle.num_threads()
+    step, fl, desc = oracle_sample(4096, cores)
+    t0 = time.perf_counter()
+    step()
+    dt = time.perf_counter() - t0
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": desc + f"; {dt:.1f} s", "seconds": round(dt, 2)}
+
+
+def run_native(args, world, rank, local):
+    na_peaks, peak_src = load_peaks()
+    R = Runner(rank)
+    cfg0 = R.cfgs[0]
+    step_flops = sum(flops(c) for c in R.cfgs)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2 (126 MB)
+
+    for _ in range(args.warmup):
+        R.step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    per_step = timed_steps(R.step, args.steps, flush)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop()
+    launches_per_step = R.launches
+    ms_rank = sum(per_step) / args.steps
+    ms = reduce_max(ms_rank, world)
+    value = world * step_flops / (ms * 1e-3) / 1e12
+
+    # fwd-only timing (for the "fwd ms" half of the metric)
+    fwd_ms = reduce_max(sum(timed_steps(R.fwd_only, max(2, args.steps // 2), flush)) /
+                        max(2, args.steps // 2), world)
+
+    # per-kernel device times, live, via the library's event hook on the launch stream
+    R.na.profile_enable(True)
+    prof_steps = 2
+    for _ in range(prof_steps):
+        flush.zero_()
+        R.step()
+    rec = R.na.profile_collect()
+    R.na.profile_enable(False)
+    per_kernel = {}
+    for name, t in rec:
+        d = per_kernel.setdefault(name, [0.0, 0])
+        d[0] += t
+        d[1] += 1
+    dominant = max(per_kernel, key=lambda n: per_kernel[n][0])
+    dom_ms, dom_n = per_kernel[dominant]
+    avg_launch_ms = dom_ms / dom_n
+    alg_bytes = algorithmic_bytes(cfg0, dominant)
+    achieved = alg_bytes / (avg_launch_ms * 1e-3) / 1e9
+    peak = float(na_peaks["hbm_gbs"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dominant)
+        except Exception:
+            traffic = None
+    shares = {n: round(v[0] / sum(x[0] for x in per_kernel.values()), 4) for n, v in per_kernel.items()}
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = [t.cpu().pin_memory() for t in (R.q, R.k, R.v, R.do)]
+        dev = [torch.empty_like(t) for t in (R.q, R.k, R.v, R.do)]
+        outs_host = [[torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                      for t in (o, lse, *g)] for (o, lse, g, _) in R.outs]
+
+        def e2e_step():
+            for h, d in zip(host, dev):
+                d.copy_(h, non_blocking=True)
+            R.step(*dev)
+            for (o, lse, g, _), hs in zip(R.outs, outs_host):
+                for src, dst in zip((o, lse, *g), hs):
+                    dst.copy_(src, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        n_e2e = max(2, min(args.steps, 5))
+        barrier(world)
+        e_ms = reduce_max(sum(timed_steps(e2e_step, n_e2e)) / n_e2e, world)
+        h2d = sum(t.numel() * t.element_size() for t in host)
+        d2h = sum(t.numel() * t.element_size() for hs in outs_host for t in hs)
+        e2e = {"value": world * step_flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_sample()
+        except Exception as ex:  # pragma: no cover
+            cpu = {"error": str(ex)}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic unit-normal Q,K,V,dO (seeded per (b,h)); no weights",
+        "config": {"workload": WORKLOAD, "variants": VARIANTS, "batch_per_gpu": cfg0.batch,
+                   "heads": cfg0.heads, "seq_len": cfg0.tokens, "head_dim": cfg0.head_dim,
+                   "kernel_size": 255, "parallelism": f"bxh-shard x{world} (weak)",
+                   "l2": "inputs 1.07 GB/step > 126 MB L2, plus a 256 MB L2 flush between steps "
+                         "outside the timed events"},
+        "fwd_ms_per_step": round(fwd_ms, 4),
+        "tensor_peak_frac": round(value / world / float(na_peaks.get("bf16_tflops", 1590.0)), 4),
+        "roofline": {"kernel": dominant, "bound": "hbm", "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src,
+                     "step_share": shares},
+        "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    cores = oracle.num_threads()
+    step, fl, desc = oracle_sample(1024, cores)
+    for _ in range(args.warmup):
+        step()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    sec = sum(ts) / len(ts)
+    value = fl / sec / 1e12
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, world, rank)
+        return
+    world, rank, local = init_dist()
+    run_native(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -130,6 +130,17 @@ const char* na_last_error(void);
  * this host thread (for the benchmark's gpu_launches count). */
 int na_last_launch_count(void);
 
+/* Benchmark instrumentation (per host thread, off by default).  While
+ * enabled, every kernel launch made by na_fwd / na_bwd on this thread is
+ * bracketed by two CUDA events recorded on the launch stream (the stream the
+ * kernel runs on).  na_profile_collect() waits for those events, writes up to
+ * `max_entries` (kernel id, device milliseconds) pairs in launch order,
+ * returns how many launches were recorded, and clears the list.  Kernel ids
+ * are named by na_kernel_name(). */
+void na_profile_enable(int on);
+int na_profile_collect(int* kernel_ids, float* ms, int max_entries);
+const char* na_kernel_name(int kernel_id);
+
 #ifdef __cplusplus
 }
 #endif

@@ -269,8 +269,10 @@ template <typename T, int DPL>
 cudaError_t launch_fwd(const Geom& g, const void* q, const void* k, const void* v, void* o,
                        float* lse, cudaStream_t st) {
   const int64_t rows = (int64_t)g.BH * g.N;
+  prof_begin(KID_FWD_SIMT, st);
   fna_fwd_simt<T, DPL><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
       g, (const T*)q, (const T*)k, (const T*)v, (T*)o, lse);
+  prof_end(st);
   return cudaGetLastError();
 }
 
@@ -280,11 +282,17 @@ cudaError_t launch_bwd(const Geom& g, const void* q, const void* k, const void* 
                        float* Dvec, cudaStream_t st) {
   const int64_t rows = (int64_t)g.BH * g.N;
   const unsigned grid = (unsigned)((rows + 7) / 8);
+  prof_begin(KID_BWD_PRE, st);
   fna_bwd_pre<T><<<grid, 256, 0, st>>>(g, (const T*)o, (const T*)d_o, Dvec);
+  prof_end(st);
+  prof_begin(KID_DKDV_SIMT, st);
   fna_dkdv_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
                                               (const T*)d_o, lse, Dvec, (T*)dk, (T*)dv);
+  prof_end(st);
+  prof_begin(KID_DQ_SIMT, st);
   fna_dq_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
                                             (const T*)d_o, lse, Dvec, (T*)dq);
+  prof_end(st);
   return cudaGetLastError();
 }
 
@@ -322,6 +330,7 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
                            cudaStream_t st) {
   const int64_t rows = (int64_t)g.BH * g.N;
   const unsigned grid = (unsigned)((rows + 7) / 8);
+  prof_begin(KID_BWD_PRE, st);
   switch (dtype) {
     case 0: fna_bwd_pre<float><<<grid, 256, 0, st>>>(g, (const float*)o, (const float*)d_o, Dvec); break;
     case 1: fna_bwd_pre<__half><<<grid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec); break;
@@ -329,6 +338,7 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
       fna_bwd_pre<__nv_bfloat16><<<grid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
                                                        (const __nv_bfloat16*)d_o, Dvec);
   }
+  prof_end(st);
   return cudaGetLastError();
 }
 

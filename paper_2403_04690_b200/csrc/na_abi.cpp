@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "na_kernels.h"
 
@@ -17,6 +18,13 @@ namespace {
 
 thread_local std::string g_last_error;
 thread_local int g_last_launches = 0;
+
+struct ProfEntry {
+  int id;
+  cudaEvent_t a, b;
+};
+thread_local bool g_prof = false;
+thread_local std::vector<ProfEntry> g_prof_list;
 
 na_status fail(na_status s, const char* fmt, ...) {
   char buf[512];
@@ -114,7 +122,52 @@ na_status cuda_status(cudaError_t e, const char* what) {
 
 }  // namespace
 
+namespace na {
+
+void prof_begin(int kernel_id, cudaStream_t st) {
+  if (!g_prof) return;
+  ProfEntry e{kernel_id, nullptr, nullptr};
+  cudaEventCreate(&e.a);
+  cudaEventCreate(&e.b);
+  cudaEventRecord(e.a, st);
+  g_prof_list.push_back(e);
+}
+
+void prof_end(cudaStream_t st) {
+  if (!g_prof || g_prof_list.empty()) return;
+  cudaEventRecord(g_prof_list.back().b, st);
+}
+
+}  // namespace na
+
 extern "C" {
+
+void na_profile_enable(int on) { g_prof = on != 0; }
+
+int na_profile_collect(int* kernel_ids, float* ms, int max_entries) {
+  const int n = (int)g_prof_list.size();
+  for (int i = 0; i < n; ++i) {
+    ProfEntry& e = g_prof_list[i];
+    float t = -1.f;
+    if (cudaEventSynchronize(e.b) == cudaSuccess) cudaEventElapsedTime(&t, e.a, e.b);
+    if (i < max_entries) {
+      if (kernel_ids) kernel_ids[i] = e.id;
+      if (ms) ms[i] = t;
+    }
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  g_prof_list.clear();
+  return n;
+}
+
+const char* na_kernel_name(int kernel_id) {
+  static const char* names[na::KID_COUNT] = {"fna_fwd_tc",  "fna_fwd_simt", "fna_bwd_pre",
+                                             "fna_dkdv_tc", "fna_dq_tc",    "fna_dkdv_simt",
+                                             "fna_dq_simt"};
+  return kernel_id >= 0 && kernel_id < na::KID_COUNT ? names[kernel_id] : "unknown";
+}
+
 
 na_status na_validate(const na_problem* p) {
   na_status s = validate(p);

@@ -6,6 +6,21 @@
 
 namespace na {
 
+// Kernel ids for the profiling hook (na_profile_*; names in na_abi.cpp).
+enum KernelId {
+  KID_FWD_TC = 0,
+  KID_FWD_SIMT = 1,
+  KID_BWD_PRE = 2,
+  KID_DKDV_TC = 3,
+  KID_DQ_TC = 4,
+  KID_DKDV_SIMT = 5,
+  KID_DQ_SIMT = 6,
+  KID_COUNT = 7
+};
+// Bracket one launch with events when profiling is enabled on this thread.
+void prof_begin(int kernel_id, cudaStream_t st);
+void prof_end(cudaStream_t st);
+
 // dtype: 0 = fp32, 1 = fp16, 2 = bf16 (matches na_dtype)
 cudaError_t simt_fwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
                      void* o, float* lse, cudaStream_t st);

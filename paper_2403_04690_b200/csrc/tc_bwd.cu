@@ -59,11 +59,11 @@ constexpr uint32_t kColS = 0, kColP = 128, kColOut = 256;
 __device__ __forceinline__ uint32_t packed_col(int kk) { return 64 * (kk >> 2) + 8 * (kk & 3); }
 
 template <int RANK, int D, bool BF16, bool KV_STATIONARY>
-__global__ void __launch_bounds__(kThreads, 1)
-    fna_bwd_tc(const __grid_constant__ CUtensorMap map_a0, const __grid_constant__ CUtensorMap map_a1,
-               const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ CUtensorMap map_b1,
-               Geom g, TcPlan pl, const float* __restrict__ lse, const float* __restrict__ dvec,
-               void* __restrict__ out0, void* __restrict__ out1) {
+__device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtensorMap& map_a1,
+                                         const CUtensorMap& map_b0, const CUtensorMap& map_b1,
+                                         const Geom& g, const TcPlan& pl, const float* __restrict__ lse,
+                                         const float* __restrict__ dvec, void* __restrict__ out0,
+                                         void* __restrict__ out1) {
   using S = BwdSmem<D>;
   using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -313,14 +313,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// dK, dV: key-stationary over the inverse halo.
+template <int RANK, int D, bool BF16>
+__global__ void __launch_bounds__(kThreads, 1)
+    fna_dkdv_tc(const __grid_constant__ CUtensorMap map_k, const __grid_constant__ CUtensorMap map_v,
+                const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_do,
+                Geom g, TcPlan pl, const float* __restrict__ lse, const float* __restrict__ dvec,
+                void* __restrict__ dk, void* __restrict__ dv) {
+  bwd_body<RANK, D, BF16, true>(map_k, map_v, map_q, map_do, g, pl, lse, dvec, dk, dv);
+}
+
+// dQ: query-stationary over the forward halo.
+template <int RANK, int D, bool BF16>
+__global__ void __launch_bounds__(kThreads, 1)
+    fna_dq_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_do,
+              const __grid_constant__ CUtensorMap map_k, const __grid_constant__ CUtensorMap map_v,
+              Geom g, TcPlan pl, const float* __restrict__ lse, const float* __restrict__ dvec,
+              void* __restrict__ dq) {
+  bwd_body<RANK, D, BF16, false>(map_q, map_do, map_k, map_v, g, pl, lse, dvec, dq, nullptr);
+}
+
 template <int RANK, int D, bool BF16>
 cudaError_t launch_both(const Geom& g, const TcPlan& pl, const CUtensorMap* m, const float* lse,
                         const float* dvec, void* dq, void* dk, void* dv, cudaStream_t st) {
   // m: [0] Q tile, [1] K tile, [2] V tile, [3] dO tile, [4] Q chunk, [5] K chunk,
   //    [6] V chunk, [7] dO chunk
   const int smem = BwdSmem<D>::kBytes + 1024;
-  auto kdkdv = fna_bwd_tc<RANK, D, BF16, true>;
-  auto kdq = fna_bwd_tc<RANK, D, BF16, false>;
+  auto kdkdv = fna_dkdv_tc<RANK, D, BF16>;
+  auto kdq = fna_dq_tc<RANK, D, BF16>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kdkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -331,10 +351,14 @@ cudaError_t launch_both(const Geom& g, const TcPlan& pl, const CUtensorMap* m, c
   }
   const long long grid = (long long)g.BH * pl.nres * pl.tiles;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  prof_begin(KID_DKDV_TC, st);
   kdkdv<<<(unsigned)grid, kThreads, smem, st>>>(m[1], m[2], m[4], m[7], g, pl, lse, dvec, dk, dv);
+  prof_end(st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  kdq<<<(unsigned)grid, kThreads, smem, st>>>(m[0], m[3], m[5], m[6], g, pl, lse, dvec, dq, nullptr);
+  prof_begin(KID_DQ_TC, st);
+  kdq<<<(unsigned)grid, kThreads, smem, st>>>(m[0], m[3], m[5], m[6], g, pl, lse, dvec, dq);
+  prof_end(st);
   return cudaGetLastError();
 }
 

@@ -264,7 +264,9 @@ cudaError_t launch(const Geom& g, const TcPlan& pl, const CUtensorMap& mq, const
   }
   const long long grid = (long long)g.BH * pl.nres * pl.tiles;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  prof_begin(KID_FWD_TC, st);
   kern<<<(unsigned)grid, kThreads, smem, st>>>(mq, mk, mv, g, pl, o, lse);
+  prof_end(st);
   return cudaGetLastError();
 }
 

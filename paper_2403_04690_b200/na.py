@@ -47,7 +47,8 @@ class NAError(RuntimeError):
 _lib = None
 
 EXPORTS = ("na_validate", "na_fwd", "na_bwd", "na_bwd_workspace_size", "na_selected_impl",
-           "na_status_string", "na_last_error", "na_last_launch_count")
+           "na_status_string", "na_last_error", "na_last_launch_count", "na_profile_enable",
+           "na_profile_collect", "na_kernel_name")
 
 
 def lib():
@@ -76,6 +77,13 @@ def lib():
         L.na_last_error.restype = ctypes.c_char_p
         L.na_last_launch_count.argtypes = []
         L.na_last_launch_count.restype = ctypes.c_int
+        L.na_profile_enable.argtypes = [ctypes.c_int]
+        L.na_profile_enable.restype = None
+        L.na_profile_collect.argtypes = [ctypes.POINTER(ctypes.c_int),
+                                         ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+        L.na_profile_collect.restype = ctypes.c_int
+        L.na_kernel_name.argtypes = [ctypes.c_int]
+        L.na_kernel_name.restype = ctypes.c_char_p
         _lib = L
     return _lib
 
@@ -139,6 +147,19 @@ def na_bwd_workspace_size(p: Problem) -> int:
 
 def last_launch_count() -> int:
     return lib().na_last_launch_count()
+
+
+def profile_enable(on: bool = True):
+    """Bracket every launch of this thread with CUDA events (benchmarking)."""
+    lib().na_profile_enable(1 if on else 0)
+
+
+def profile_collect(max_entries: int = 4096):
+    """[(kernel name, device ms), ...] for the launches since the last collect."""
+    ids = (ctypes.c_int * max_entries)()
+    ms = (ctypes.c_float * max_entries)()
+    n = lib().na_profile_collect(ids, ms, max_entries)
+    return [(lib().na_kernel_name(ids[i]).decode(), float(ms[i])) for i in range(min(n, max_entries))]
 
 
 def na_fwd(q, k, v, kernel_size, dilation=None, is_causal=None, scale=None, impl="auto",
