@@ -37,9 +37,9 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    extra = ["-Xptxas", "-v"] if verbose else []
+def _compile(src: str, verbose: bool, bdir: str = BUILD, trace: bool = False) -> str:
+    obj = os.path.join(bdir, os.path.basename(src) + ".o")
+    extra = (["-Xptxas", "-v"] if verbose else []) + (["-DNA_TRACE"] if trace else [])
     cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -49,20 +49,24 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """libna.so (or, with trace=True, the timeline-instrumented libna_trace.so
+    used only for kernel studies; the product never loads it)."""
+    out = OUT if not trace else os.path.join(PKG, "libna_trace.so")
+    if not trace and not force and up_to_date():
         return OUT
-    os.makedirs(BUILD, exist_ok=True)
+    bdir = BUILD if not trace else BUILD + "_trace"
+    os.makedirs(bdir, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), sources()))
-    tmp = OUT + f".{os.getpid()}.tmp"
+        objs = list(ex.map(lambda s: _compile(s, verbose, bdir, trace), sources()))
+    tmp = out + f".{os.getpid()}.tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -32,6 +32,9 @@ template <> __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float x)
   return __float2bfloat16_rn(x);
 }
 
+__device__ __forceinline__ float ld_val(__half x) { return __half2float(x); }
+__device__ __forceinline__ float ld_val(__nv_bfloat16 x) { return __bfloat162float(x); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -134,6 +137,30 @@ __global__ void __launch_bounds__(256) fna_bwd_pre(Geom g, const T* __restrict__
   for (int d = lane; d < g.D; d += 32) s = fmaf(ld(o + row * g.D + d), ld(d_o + row * g.D + d), s);
   s = warp_sum(s);
   if (lane == 0) Dvec[row] = s;
+}
+
+// D_x for 16-bit rows: each thread reads 16 bytes (8 elements) of O and dO,
+// D/8 consecutive threads own a row and reduce with shuffles (fully
+// coalesced 16-byte loads; the kernel is HBM-bound).
+template <typename T>
+__global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restrict__ o,
+                                                       const T* __restrict__ d_o,
+                                                       float* __restrict__ Dvec) {
+  const int tpr = g.D / 8;  // threads per row (power of two: D in {8,...,256} multiple of 8)
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / tpr;
+  const int part = (int)(gid % tpr);
+  float s = 0.f;
+  if (row < (int64_t)g.BH * g.N) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + row * g.D) + part);
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(d_o + row * g.D) + part);
+    const T* ea = reinterpret_cast<const T*>(&a);
+    const T* eb = reinterpret_cast<const T*>(&b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s = fmaf(ld_val(ea[i]), ld_val(eb[i]), s);
+  }
+  for (int off = 1; off < tpr; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (part == 0 && row < (int64_t)g.BH * g.N) Dvec[row] = s;
 }
 
 // ------------------------------------------------------------- bwd: dQ
@@ -331,12 +358,15 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
   const int64_t rows = (int64_t)g.BH * g.N;
   const unsigned grid = (unsigned)((rows + 7) / 8);
   prof_begin(KID_BWD_PRE, st);
+  const unsigned vgrid = (unsigned)((rows * (g.D / 8) + 255) / 256);
   switch (dtype) {
     case 0: fna_bwd_pre<float><<<grid, 256, 0, st>>>(g, (const float*)o, (const float*)d_o, Dvec); break;
-    case 1: fna_bwd_pre<__half><<<grid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec); break;
+    case 1:
+      fna_bwd_pre_vec<__half><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec);
+      break;
     default:
-      fna_bwd_pre<__nv_bfloat16><<<grid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
-                                                       (const __nv_bfloat16*)d_o, Dvec);
+      fna_bwd_pre_vec<__nv_bfloat16><<<vgrid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
+                                                            (const __nv_bfloat16*)d_o, Dvec);
   }
   prof_end(st);
   return cudaGetLastError();

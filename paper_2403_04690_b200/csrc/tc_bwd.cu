@@ -9,15 +9,18 @@
 //   fna_dkdv_tc  key-stationary: a CTA owns 128 keys of one residue class and
 //                streams the query chunks of the tile's INVERSE halo
 //                [inv_start(y_lo), inv_end(y_hi)] (the IN gather pattern,
-//                P:253-258).  Per chunk: S^T = K Q^T and dP^T = V dO^T (SS MMAs),
-//                P^T = exp(scale S^T - LSE_q), dS^T = P^T (dP^T - D_q) by the
-//                compute warps (written back to TMEM as 16-bit), then
-//                dV += P^T dO and dK += dS^T Q (TS MMAs, accumulators in TMEM).
+//                P:253-258).  Per 64-query sub-chunk: S^T = K Q^T and
+//                dP^T = V dO^T (SS MMAs), P^T = exp(scale S^T - LSE_q) and
+//                dS^T = P^T (dP^T - D_q) by the compute warps (written back to
+//                TMEM as 16-bit), then dV += P^T dO and dK += dS^T Q (TS MMAs).
 //   fna_dq_tc    query-stationary over the forward halo: S = Q K^T, dP = dO V^T,
 //                dS = P (dP - D), dQ += dS K.
 // Warp roles (320 threads, 1 CTA per SM): warp 0 TMA producer, warp 1 TMEM
-// owner + single-thread MMA issuer, warps 2..9 compute (thread = TMEM lane =
-// stationary row; warps w and w+4 split the chunk's 128 columns in halves).
+// owner + single-thread MMA issuer, warps 2..9 two compute warpgroups
+// (thread = TMEM lane = stationary row).  Sub-chunk u lives in TMEM buffer
+// u%2 and is processed by warpgroup u%2, so the tensor core computes
+// sub-chunk u+1 while warpgroup u%2 works on u (ping-pong):
+//   MMA order: ST_0, ST_1, [P_0] OUT_0, ST_2, [P_1] OUT_1, ST_3, ...
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -33,7 +36,6 @@ namespace {
 
 constexpr int kStages = 2;
 constexpr int kThreads = 320;
-constexpr int kCompute = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
@@ -44,19 +46,24 @@ struct BwdSmem {
   static constexpr int kA1 = kA0 + kTile;             // stationary tile 1 (V | dO)
   static constexpr int kB0 = kA1 + kTile;             // streamed [kStages] (Q | K)
   static constexpr int kB1 = kB0 + kStages * kTile;   // streamed [kStages] (dO | V)
-  static constexpr int kVec = kB1 + kStages * kTile;  // [2][2][128] fp32 (LSE2, D) staging
+  static constexpr int kVec = kB1 + kStages * kTile;  // [group][slot][LSE2 x64 | D x64] fp32
   static constexpr int kBar = kVec + 2 * 2 * 128 * 4;
   static constexpr int kBytes = kBar + 256;
 };
 
-// TMEM columns: [0,128) S-like accumulator, [128,256) dP-like accumulator,
-// [256, 256+D) first output, [256+D, 256+2D) second output (dK/dV kernel).
+// TMEM columns: [0,128) two 64-column S-like buffers, [128,256) two dP-like
+// buffers, [256, 256+D) first output, [256+D, 256+2D) second output.
 constexpr uint32_t kColS = 0, kColP = 128, kColOut = 256;
 
-// TMEM column of the 16-bit operand for MMA k-step kk (16 partner columns):
-// each 64-column half of a chunk writes its packed values inside the columns
-// it read, so the two warps sharing a TMEM lane quarter never race.
-__device__ __forceinline__ uint32_t packed_col(int kk) { return 64 * (kk >> 2) + 8 * (kk & 3); }
+enum : int {
+  B_A = 0,                  // stationary tiles loaded
+  B_B = 1,                  // streamed stage full [kStages]
+  B_E = B_B + kStages,      // streamed stage empty [kStages]
+  B_S = B_E + kStages,      // S and dP of a sub-chunk ready [2]
+  B_P = B_S + 2,            // packed operands of a sub-chunk written [2] (128 arrivals)
+  B_O = B_P + 2,            // outputs final
+  B_COUNT = B_O + 1
+};
 
 template <int RANK, int D, bool BF16, bool KV_STATIONARY>
 __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtensorMap& map_a1,
@@ -68,30 +75,28 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
   using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
-  uint64_t* bar_a = bars + 0;                  // stationary tiles loaded
-  uint64_t* bar_b = bars + 1;                  // streamed stage full [kStages]
-  uint64_t* bar_e = bars + 1 + kStages;        // streamed stage empty [kStages]
-  uint64_t* bar_s = bars + 1 + 2 * kStages;    // S and dP accumulators ready
-  uint64_t* bar_p = bar_s + 1;                 // packed operands written (256 arrivals)
-  uint64_t* bar_o = bar_s + 2;                 // outputs final
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 3);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + B_COUNT);
   float* vec = reinterpret_cast<float*>(smem + S::kVec);
 
   TileCtx<RANK> t;
   if (!t.init(g, pl, blockIdx.x, /*inverse=*/KV_STATIONARY)) return;
   const int nchunks = t.nchunks;
+  const int ns = pl.n_kv > 64 ? 2 : 1;
+  const int nsub = nchunks * ns;
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(bar_a, 1);
+    ptx::mbar_init(bar + B_A, 1);
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(bar_b + s, 1);
-      ptx::mbar_init(bar_e + s, 1);
+      ptx::mbar_init(bar + B_B + s, 1);
+      ptx::mbar_init(bar + B_E + s, 1);
     }
-    ptx::mbar_init(bar_s, 1);
-    ptx::mbar_init(bar_p, kCompute);
-    ptx::mbar_init(bar_o, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(bar + B_S + b, 1);
+      ptx::mbar_init(bar + B_P + b, 128);
+    }
+    ptx::mbar_init(bar + B_O, 1);
     ptx::fence_barrier_init();
   }
   if (pl.rows_kv < 128) {  // rows no TMA box writes must be finite (zero)
@@ -110,89 +115,103 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
+    // ===================== TMA producer (whole warp, one lane issues) =====================
+    {
       ptx::tma_prefetch(&map_a0);
       ptx::tma_prefetch(&map_a1);
       ptx::tma_prefetch(&map_b0);
       ptx::tma_prefetch(&map_b1);
-      ptx::mbar_expect_tx(bar_a, 2 * 128 * S::kRowBytes);
+      ptx::mbar_expect_tx_w(bar + B_A, 2 * 128 * S::kRowBytes);
       for (int i = 0; i < pl.q_issues; ++i) {
-        t.template load_box<RANK>(&map_a0, smem + S::kA0 + i * pl.q_box_x * S::kRowBytes, bar_a,
+        t.template load_box<RANK>(&map_a0, smem + S::kA0 + i * pl.q_box_x * S::kRowBytes, bar + B_A,
                                   t.q_origin, i * pl.q_box_x, g);
-        t.template load_box<RANK>(&map_a1, smem + S::kA1 + i * pl.q_box_x * S::kRowBytes, bar_a,
+        t.template load_box<RANK>(&map_a1, smem + S::kA1 + i * pl.q_box_x * S::kRowBytes, bar + B_A,
                                   t.q_origin, i * pl.q_box_x, g);
       }
       const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes;
       for (int j = 0; j < nchunks; ++j) {
         const int s = j % kStages;
-        if (j >= kStages) ptx::mbar_wait(bar_e + s, ((j / kStages) - 1) & 1);
+        if (j >= kStages) ptx::mbar_wait(bar + B_E + s, ((j / kStages) - 1) & 1);
         int org[3];
         t.chunk_origin(pl, j, org);
-        ptx::mbar_expect_tx(bar_b + s, bytes);
+        ptx::mbar_expect_tx_w(bar + B_B + s, bytes);
         for (int i = 0; i < pl.kv_issues; ++i) {
           t.template load_box<RANK>(&map_b0, smem + S::kB0 + s * S::kTile + i * pl.kv_box_x * S::kRowBytes,
-                                    bar_b + s, org, i * pl.kv_box_x, g);
+                                    bar + B_B + s, org, i * pl.kv_box_x, g);
           t.template load_box<RANK>(&map_b1, smem + S::kB1 + s * S::kTile + i * pl.kv_box_x * S::kRowBytes,
-                                    bar_b + s, org, i * pl.kv_box_x, g);
+                                    bar + B_B + s, org, i * pl.kv_box_x, g);
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (whole warp, one lane issues) =====================
+    {
       constexpr uint32_t kSw = D == 64 ? 2u : 4u;
       constexpr uint32_t kSbo = 8 * S::kRowBytes;
-      const uint32_t idesc_s = ptx::make_idesc(128, pl.n_kv, BF16, false);
+      const int n1 = pl.n_kv - 64;
+      const uint32_t idesc_s0 = ptx::make_idesc(128, ns == 2 ? 64 : pl.n_kv, BF16, false);
+      const uint32_t idesc_s1 = ptx::make_idesc(128, ns == 2 ? n1 : 16, BF16, false);
       constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
       const uint32_t a0 = ptx::smem_u32(smem + S::kA0), a1 = ptx::smem_u32(smem + S::kA1);
-      ptx::mbar_wait(bar_a, 0);
-      for (int j = 0; j < nchunks; ++j) {
-        const int s = j % kStages;
-        const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile);
-        const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile);
-        ptx::mbar_wait(bar_b + s, (j / kStages) & 1);
-        ptx::tc_fence_after();
+      auto issue_st = [&](int u) {
+        const int j = u / ns, h = u % ns, s = j % kStages;
+        if (h == 0) {
+          ptx::mbar_wait(bar + B_B + s, (j / kStages) & 1);
+          ptx::tc_fence_after();
+        }
+        const uint32_t off = h * 64 * S::kRowBytes;
+        const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
+        const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
+        const uint32_t id = h ? idesc_s1 : idesc_s0;
+        const uint32_t buf = (u & 1) * 64;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
-          ptx::mma_ss(tmem + kColS, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
-                      ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), idesc_s, kk > 0);
-          ptx::mma_ss(tmem + kColP, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
-                      ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), idesc_s, kk > 0);
+          ptx::mma_ss_w(tmem + kColS + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
+                      ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
+          ptx::mma_ss_w(tmem + kColP + buf, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
+                      ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
         }
-        ptx::mma_commit(bar_s);
-        ptx::mbar_wait(bar_p, j & 1);
+        ptx::mma_commit_w(bar + B_S + (u & 1));
+      };
+      ptx::mbar_wait(bar + B_A, 0);
+      issue_st(0);
+      if (nsub > 1) issue_st(1);
+      for (int u = 0; u < nsub; ++u) {
+        const int j = u / ns, h = u % ns, s = j % kStages;
+        const int width = h ? n1 : (ns == 2 ? 64 : pl.n_kv);
+        const uint32_t off = h * 64 * S::kRowBytes;
+        const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
+        const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
+        const uint32_t buf = (u & 1) * 64;
+        ptx::mbar_wait(bar + B_P + (u & 1), (u >> 1) & 1);
         ptx::tc_fence_after();
-        for (int kk = 0; kk < pl.n_kv / 16; ++kk) {
-          const uint32_t pc = packed_col(kk);
+        for (int kk = 0; kk < width / 16; ++kk) {
           const uint32_t boff = kk * 16 * S::kRowBytes;
+          const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
           if constexpr (KV_STATIONARY) {
             // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
-            ptx::mma_ts(tmem + kColOut + D, tmem + kColS + pc,
-                        ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o,
-                        (j > 0 || kk > 0) ? 1u : 0u);
-            ptx::mma_ts(tmem + kColOut, tmem + kColP + pc,
-                        ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o,
-                        (j > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_ts_w(tmem + kColOut + D, tmem + kColS + buf + kk * 8,
+                        ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+            ptx::mma_ts_w(tmem + kColOut, tmem + kColP + buf + kk * 8,
+                        ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
           } else {
             // dQ += dS K
-            ptx::mma_ts(tmem + kColOut, tmem + kColS + pc,
-                        ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o,
-                        (j > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_ts_w(tmem + kColOut, tmem + kColS + buf + kk * 8,
+                        ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
           }
         }
-        ptx::mma_commit(bar_e + s);
+        if (h == ns - 1) ptx::mma_commit_w(bar + B_E + s);
+        if (u + 2 < nsub) issue_st(u + 2);
       }
-      ptx::mma_commit(bar_o);
+      ptx::mma_commit_w(bar + B_O);
     }
   } else {
-    // ===================== compute warps (256 threads) =====================
-    const int cw = warp - 2;             // 0..7
+    // ===================== compute warpgroups (2 x 128 threads) =====================
+    const int grp = (warp - 2) >> 2;     // processes sub-chunks u with u % 2 == grp
     const int quarter = warp & 3;
-    const int half = cw >> 2;            // which 64 columns of a chunk
     const int row = quarter * 32 + lane;
-    const int ctid = cw * 32 + lane;     // 0..255
+    const int gtid = ((warp - 2) & 3) * 32 + lane;  // 0..127 within the group
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     RowCtx<RANK> r;
     r.init(g, pl, t, row, /*inverse=*/KV_STATIONARY);
@@ -205,85 +224,102 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
         row_d = dvec[tok];
       }
     }
-    for (int j = 0; j < nchunks; ++j) {
+    uint32_t mw[4] = {0u, 0u, 0u, 0u};
+    int it = 0;
+    for (int u = grp; u < nsub; u += 2, ++it) {
+      const int j = u / ns, h = u % ns;
       int org[3];
       t.chunk_origin(pl, j, org);
-      uint32_t mw[4];
       r.chunk_mask(pl, org, mw);
-      float* cv = vec + (j & 1) * 256;   // [LSE2 x128 | D x128] of this chunk's columns
+      const uint32_t w0 = h ? mw[2] : mw[0], w1 = h ? mw[3] : mw[1];
+      float* cv = vec + (grp * 2 + (it & 1)) * 128;  // [LSE2 x64 | D x64] of this sub-chunk's columns
       if constexpr (KV_STATIONARY) {
-        // stage the partner (query) LSE and D values of this chunk's columns
-        const int col = ctid & 127, which = ctid >> 7;
+        // stage the partner (query) LSE and D values of this sub-chunk's columns
+        const int col = gtid & 63, which = gtid >> 6;
+        const int ccol = h * 64 + col;  // column within the chunk
         float val = 0.f;
-        if (col < pl.rows_kv) {
-          int cc[3], rem = col;
+        if (ccol < pl.rows_kv) {
+          int rem = ccol;
           bool ok = true;
           long long tok = 0;
 #pragma unroll
           for (int a = 2; a >= 0; --a) {
             if (a >= RANK) continue;
-            cc[a] = org[a] + rem % pl.ckv[a];
+            const int cc = org[a] + rem % pl.ckv[a];
             rem /= pl.ckv[a];
-            ok = ok && cc[a] < t.Lr[a];
-            tok += (long long)(t.r[a] + g.dil[a] * cc[a]) * g.tstride[a];
+            ok = ok && cc < t.Lr[a];
+            tok += (long long)(t.r[a] + g.dil[a] * cc) * g.tstride[a];
           }
           if (ok) {
             tok += (long long)t.bh * g.N;
             val = which == 0 ? lse[tok] * kLog2e : dvec[tok];
           }
         }
-        cv[which * 128 + col] = val;
-        ptx::named_bar_sync(1, kCompute);
+        cv[which * 64 + col] = val;
+        ptx::named_bar_sync(1 + grp, 128);
       }
-      ptx::mbar_wait(bar_s, j & 1);
+      const uint32_t buf = (u & 1) * 64;
+      ptx::mbar_wait(bar + B_S + (u & 1), (u >> 1) & 1);
       ptx::tc_fence_after();
+      uint32_t pk_p[32], pk_s[32];
 #pragma unroll
       for (int gq = 0; gq < 2; ++gq) {
-        const int c0 = half * 64 + gq * 32;
+        const uint32_t w = gq ? w1 : w0;
+        if (!__any_sync(0xffffffffu, w != 0u)) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk_p[16 * gq + c] = pk_s[16 * gq + c] = 0u;
+          continue;
+        }
+        const bool full = __all_sync(0xffffffffu, w == 0xffffffffu);
         uint32_t sv[32], pv[32];
-        NA_TMEM_LD32(trow + kColS + c0, sv);
-        NA_TMEM_LD32(trow + kColP + c0, pv);
+        NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
+        NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
         ptx::tmem_ld_wait();
-        const uint32_t bits = mw[c0 >> 5];
-        uint32_t pk_p[16], pk_s[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
-          float p2[2], ds2[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int cc = c + e;
-            const float lse2 = KV_STATIONARY ? cv[c0 + cc] : row_lse2;
-            const float dd = KV_STATIONARY ? cv[128 + c0 + cc] : row_d;
-            const float p = (bits >> cc) & 1u ? ptx::ex2(__uint_as_float(sv[cc]) * sl2 - lse2) : 0.f;
-            p2[e] = p;
-            ds2[e] = p * (__uint_as_float(pv[cc]) - dd);
+          float2 nl, dd;
+          if constexpr (KV_STATIONARY) {
+            nl = make_float2(-cv[32 * gq + c], -cv[32 * gq + c + 1]);
+            dd = make_float2(cv[64 + 32 * gq + c], cv[64 + 32 * gq + c + 1]);
+          } else {
+            nl = make_float2(-row_lse2, -row_lse2);
+            dd = make_float2(row_d, row_d);
           }
-          pk_p[c >> 1] = pack2<BF16>(p2[0], p2[1]);
-          pk_s[c >> 1] = pack2<BF16>(ds2[0], ds2[1]);
+          float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])),
+                                make_float2(sl2, sl2), nl);
+          if (!full) {
+            x.x = (w >> c) & 1u ? x.x : -INFINITY;
+            x.y = (w >> (c + 1)) & 1u ? x.y : -INFINITY;
+          }
+          const float2 p = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+          const float2 ds = __fmul2_rn(p, __fadd2_rn(make_float2(__uint_as_float(pv[c]),
+                                                                 __uint_as_float(pv[c + 1])),
+                                                     make_float2(-dd.x, -dd.y)));
+          pk_p[16 * gq + (c >> 1)] = pack2<BF16>(p.x, p.y);
+          pk_s[16 * gq + (c >> 1)] = pack2<BF16>(ds.x, ds.y);
         }
-        const uint32_t pc = 64 * half + 16 * gq;  // == packed_col(kk) for this group's kk
-        if constexpr (KV_STATIONARY) {
-          NA_TMEM_ST16(trow + kColS + pc, pk_p);
-          NA_TMEM_ST16(trow + kColP + pc, pk_s);
-        } else {
-          NA_TMEM_ST16(trow + kColS + pc, pk_s);
-        }
+      }
+      if constexpr (KV_STATIONARY) {
+        NA_TMEM_ST32(trow + kColS + buf, pk_p);  // P^T  -> A of dV += P^T dO
+        NA_TMEM_ST32(trow + kColP + buf, pk_s);  // dS^T -> A of dK += dS^T Q
+      } else {
+        NA_TMEM_ST32(trow + kColS + buf, pk_s);  // dS -> A of dQ += dS K
       }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(bar_p);
+      ptx::mbar_arrive(bar + B_P + (u & 1));
     }
     // ---- epilogue ----
-    ptx::mbar_wait(bar_o, 0);
+    ptx::mbar_wait(bar + B_O, 0);
     ptx::tc_fence_after();
-    // KV-stationary: half 0 writes dK (x scale), half 1 writes dV.  Q-stationary:
-    // the two halves split dQ's D columns.
+    // KV-stationary: group 0 writes dK (x scale), group 1 writes dV.
+    // Q-stationary: the two groups split dQ's D columns.
     const long long off = r.out_offset(g, t);
     constexpr int kCols = KV_STATIONARY ? D : D / 2;
-    const uint32_t src = KV_STATIONARY ? kColOut + half * D : kColOut + half * (D / 2);
-    T* dst = reinterpret_cast<T*>(KV_STATIONARY && half ? out1 : out0) + off +
-             (KV_STATIONARY ? 0 : half * (D / 2));
-    const float mul = (KV_STATIONARY && half) ? 1.f : g.scale;
+    const uint32_t src = KV_STATIONARY ? kColOut + grp * D : kColOut + grp * (D / 2);
+    T* dst = reinterpret_cast<T*>(KV_STATIONARY && grp ? out1 : out0) + off +
+             (KV_STATIONARY ? 0 : grp * (D / 2));
+    const float mul = (KV_STATIONARY && grp) ? 1.f : g.scale;
 #pragma unroll
     for (int c0 = 0; c0 < kCols; c0 += 16) {
       uint32_t ov[16];

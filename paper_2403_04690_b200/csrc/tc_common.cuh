@@ -15,6 +15,7 @@ namespace na {
 
 // Host side (tc_host.cpp).
 TcPlan make_plan(const Geom& g, int tile_rows);
+int num_sms();  // SMs of the current device (cached per device)
 cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base,
                      const int box[3], int box_x);
 
@@ -27,6 +28,27 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
+}
+
+// 2^x for a pair of values on the FMA pipe (the MUFU ex2 unit is the
+// scarcest resource of the softmax): Cody-Waite split x = n + f with
+// n = rint(x), f in [-0.5, 0.5]; 2^f by a degree-3 polynomial with c0 = 1
+// exactly (relative error 1.1e-4, below half an fp16 ulp; P is rounded to
+// 16 bits before the PV MMA); 2^n is added to the exponent field.  x is
+// clamped to >= -127 so a masked logit (-inf) yields +0 (n = -127, f = 0).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  constexpr float kC1 = 0.6933686137f, kC2 = 0.2422178388f, kC3 = 0.0545928255f;
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));  // 1.5*2^23: rint in low bits
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-n.x, -n.y));
+  float2 p = __ffma2_rn(f, make_float2(kC3, kC3), make_float2(kC2, kC2));
+  p = __ffma2_rn(p, f, make_float2(kC1, kC1));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  const int ex = (__float_as_int(t.x) - 0x4B400000) << 23;
+  const int ey = (__float_as_int(t.y) - 0x4B400000) << 23;
+  return make_float2(__int_as_float(__float_as_int(p.x) + ex), __int_as_float(__float_as_int(p.y) + ey));
 }
 
 // Which (b*h, residue class, tile) a CTA owns, and the tile's halo.
@@ -47,10 +69,11 @@ struct TileCtx {
 
   __device__ __forceinline__ bool init(const Geom& g, const TcPlan& pl, unsigned block,
                                        bool inverse = false) {
-    int tile = (int)(block % (unsigned)pl.tiles);
-    unsigned rest = block / (unsigned)pl.tiles;
-    int res = (int)(rest % (unsigned)pl.nres);
-    bh = (int)(rest / (unsigned)pl.nres);
+    const uint32_t rest = fdiv(block, pl.f_tiles);
+    uint32_t tile = block - rest * pl.f_tiles.d;
+    const uint32_t bhq = fdiv(rest, pl.f_nres);
+    uint32_t res = rest - bhq * pl.f_nres.d;
+    bh = (int)bhq;
     nchunks = 1;
 #pragma unroll
     for (int a = 2; a >= 0; --a) {
@@ -58,11 +81,13 @@ struct TileCtx {
         r[a] = 0; Lr[a] = 1; q_origin[a] = 0; qv[a] = 1; lo[a] = 0; nch[a] = 1;
         continue;
       }
-      r[a] = res % g.dil[a];
-      res /= g.dil[a];
-      const int ti = tile % pl.ntile[a];
-      tile /= pl.ntile[a];
-      Lr[a] = class_size(g.L[a], g.dil[a], r[a]);
+      const uint32_t rq = fdiv(res, pl.f_dil[a]);
+      r[a] = (int)(res - rq * pl.f_dil[a].d);
+      res = rq;
+      const uint32_t tq_ = fdiv(tile, pl.f_ntile[a]);
+      const int ti = (int)(tile - tq_ * pl.f_ntile[a].d);
+      tile = tq_;
+      Lr[a] = (int)fdiv((uint32_t)(g.L[a] - r[a] + g.dil[a] - 1), pl.f_dil[a]);
       q_origin[a] = ti * pl.tq[a];
       qv[a] = min(pl.tq[a], Lr[a] - q_origin[a]);
       int hi;
@@ -87,8 +112,12 @@ struct TileCtx {
 #pragma unroll
     for (int a = 2; a >= 0; --a) {
       if (a >= RANK) { org[a] = 0; continue; }
-      org[a] = lo[a] + (rem % nch[a]) * pl.ckv[a];
-      rem /= nch[a];
+      if (a == 0) {  // outermost axis: rem < nch[0] already
+        org[a] = lo[a] + rem * pl.ckv[a];
+      } else {
+        org[a] = lo[a] + (rem % nch[a]) * pl.ckv[a];
+        rem /= nch[a];
+      }
     }
   }
 
@@ -99,12 +128,12 @@ struct TileCtx {
   __device__ __forceinline__ void load_box(const CUtensorMap* m, void* dst, uint64_t* bar,
                                            const int org[3], int x_off, const Geom& g) const {
     if constexpr (R == 1) {
-      ptx::tma_load_3d(dst, m, bar, 0, r[0] + g.dil[0] * (org[0] + x_off), bh);
+      ptx::tma_load_3d_w(dst, m, bar, 0, r[0] + g.dil[0] * (org[0] + x_off), bh);
     } else if constexpr (R == 2) {
-      ptx::tma_load_4d(dst, m, bar, 0, r[1] + g.dil[1] * (org[1] + x_off),
+      ptx::tma_load_4d_w(dst, m, bar, 0, r[1] + g.dil[1] * (org[1] + x_off),
                        r[0] + g.dil[0] * org[0], bh);
     } else {
-      ptx::tma_load_5d(dst, m, bar, 0, r[2] + g.dil[2] * (org[2] + x_off),
+      ptx::tma_load_5d_w(dst, m, bar, 0, r[2] + g.dil[2] * (org[2] + x_off),
                        r[1] + g.dil[1] * org[1], r[0] + g.dil[0] * org[0], bh);
     }
   }
@@ -136,8 +165,8 @@ struct RowCtx {
 #pragma unroll
     for (int a = 2; a >= 0; --a) {
       if (a >= RANK) { c[a] = 0; wlo[a] = 0; whi[a] = 0; continue; }
-      const int off = rem % pl.tq[a];
-      rem /= pl.tq[a];
+      const int off = rem & (pl.tq[a] - 1);  // tile extents are powers of two
+      rem >>= pl.tq_shift[a];
       c[a] = t.q_origin[a] + off;
       valid = valid && off < t.qv[a];
       if (!inverse) {

@@ -1,20 +1,29 @@
 // tc_fwd.cu — fused neighborhood attention forward on sm_100a tensor cores.
 //
-// One CTA = one 128-query multi-dimensional tile of one residue class of one
-// (b, h) (§3.3 fused NA, Fig. 4; dilation as extra CTAs P:329-331).
-// Warp roles (192 threads, 2 CTAs per SM):
-//   warp 0      TMA producer: Q box once, then K and V boxes of every KV chunk
-//               of the tile's halo (a 2-stage mbarrier ring).
-//   warp 1      TMEM owner + single-thread tcgen05.mma issuer:
-//                 S = Q K^T  (SS, fp32 accumulate in TMEM cols [0,128))
-//                 O += P V   (TS: P read from TMEM cols [0,64), V MN-major)
-//   warps 2..5  softmax: thread = query row = TMEM lane.  tcgen05.ld its S
-//               row, applies the neighborhood mask (per-row window bitmask,
-//               P:295), online softmax in the log2 domain with lazy
-//               O rescaling, writes P (16-bit) back into TMEM,
-//               and finally normalizes O and stores O and LSE.
-// Only chunks of the tile's halo box [start(q_lo), end(q_hi)] are visited
-// (tile skipping: every other KV tile has no key in any row's window).
+// One CTA handles 128-query multi-dimensional tiles, each of one residue
+// class of one (b, h) (§3.3 fused NA, Fig. 4; dilation as extra
+// tiles P:329-331).  Persistent: 2 CTAs per SM walk the tile list
+// blockIdx.x, blockIdx.x + gridDim.x, ...  Warp roles (192 threads):
+//   warp 0      TMA producer: Q box per tile (double-buffered), then K and V
+//               boxes of every KV chunk of the tile's halo (2-stage ring).
+//   warp 1      TMEM owner + MMA issuer (whole warp, one elected lane).
+//   warps 2..5  softmax + epilogue: thread = query row = TMEM lane.
+// Each KV chunk (<= 128 keys, one TMA box) is consumed as <= 2 sub-chunks of
+// 64 keys whose S = Q K^T accumulators alternate between two TMEM buffers, so
+// the tensor core computes sub-chunk u+1 (and PV of u-1) while the softmax
+// warps work on sub-chunk u:
+//   MMA order per tile: S_0, S_1, [P_0] PV_0, S_2, [P_1] PV_1, S_3, ...
+//   (S_{u+2} reuses the buffer PV_u reads; tcgen05 ops from one thread run
+//   in issue order.)  O is double-buffered in TMEM so the epilogue of tile i
+//   overlaps the MMAs of tile i+1.
+// Softmax per sub-chunk: tcgen05.ld the row's 64 logits, neighborhood mask
+// (per-row window bitmask) applied only to 32-column groups
+// that are partially valid for the warp, groups with no valid key skipped,
+// online softmax in the log2 domain with lazy O rescaling, P
+// written back to TMEM as 16-bit (A operand of PV).  The exponentials are
+// split between the MUFU unit (ex2.approx) and a Cody-Waite polynomial on
+// the FMA pipe (packed FFMA2), since MUFU throughput bounds this kernel.
+// Only chunks of the tile's halo box [start(q_lo), end(q_hi)] are visited.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -30,53 +39,64 @@ namespace {
 
 constexpr int kStages = 2;
 constexpr int kThreads = 192;
+constexpr int kSoftmax = 128;    // softmax threads (warps 2..5)
+constexpr uint32_t kColO = 128;  // O accumulators: [128, 128+D) and [128+D, 128+2D)
 
 template <int D>
 struct FwdSmem {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTile = 128 * kRowBytes;  // Q tile, or one K/V stage
-  static constexpr int kQ = 0;
-  static constexpr int kK = kQ + kTile;
+  static constexpr int kQ = 0;                   // [2] (double-buffered across tiles)
+  static constexpr int kK = kQ + 2 * kTile;
   static constexpr int kV = kK + kStages * kTile;
   static constexpr int kBar = kV + kStages * kTile;
   static constexpr int kBytes = kBar + 256;
+};
+
+// Barrier slots.
+enum : int {
+  B_QF = 0,                 // Q buffer full [2]
+  B_QE = B_QF + 2,          // Q buffer empty [2]
+  B_K = B_QE + 2,           // [kStages]
+  B_V = B_K + kStages,      // [kStages]
+  B_E = B_V + kStages,      // K/V stage empty [kStages]
+  B_S = B_E + kStages,      // S sub-chunk ready [2]
+  B_P = B_S + 2,            // P sub-chunk written [2] (128 arrivals)
+  B_PV = B_P + 2,           // one completion per PV sub-chunk
+  B_OF = B_PV + 1,          // O buffer full [2]
+  B_OE = B_OF + 2,          // O buffer drained by the epilogue [2] (128 arrivals)
+  B_COUNT = B_OE + 2
 };
 
 template <int RANK, int D, bool BF16>
 __global__ void __launch_bounds__(kThreads, 2)
     fna_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                const __grid_constant__ CUtensorMap map_v, Geom g, TcPlan pl, void* __restrict__ o_ptr,
-               float* __restrict__ lse) {
+               float* __restrict__ lse, unsigned num_tiles) {
   using S = FwdSmem<D>;
   using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
-  uint64_t* bar_q = bars + 0;
-  uint64_t* bar_k = bars + 1;                 // [kStages]
-  uint64_t* bar_v = bars + 1 + kStages;       // [kStages]
-  uint64_t* bar_e = bars + 1 + 2 * kStages;   // kv stage empty [kStages]
-  uint64_t* bar_s = bars + 1 + 3 * kStages;   // S ready in TMEM
-  uint64_t* bar_p = bar_s + 1;                // P written to TMEM (128 arrivals)
-  uint64_t* bar_o = bar_s + 2;                // final O ready
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 3);
-
-  // ---- which tile is this CTA -------------------------------------------
-  TileCtx<RANK> t;
-  if (!t.init(g, pl, blockIdx.x)) return;  // tile beyond a ragged class: no work
-  const int nchunks = t.nchunks;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + B_COUNT);
+  const int ns = pl.n_kv > 64 ? 2 : 1;  // sub-chunks per chunk
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   if (threadIdx.x == 0) {
-    ptx::mbar_init(bar_q, 1);
-    for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(bar_k + s, 1);
-      ptx::mbar_init(bar_v + s, 1);
-      ptx::mbar_init(bar_e + s, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(bar + B_QF + b, 1);
+      ptx::mbar_init(bar + B_QE + b, 1);
+      ptx::mbar_init(bar + B_S + b, 1);
+      ptx::mbar_init(bar + B_P + b, kSoftmax);
+      ptx::mbar_init(bar + B_OF + b, 1);
+      ptx::mbar_init(bar + B_OE + b, kSoftmax);
     }
-    ptx::mbar_init(bar_s, 1);
-    ptx::mbar_init(bar_p, 128);
-    ptx::mbar_init(bar_o, 1);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(bar + B_K + s, 1);
+      ptx::mbar_init(bar + B_V + s, 1);
+      ptx::mbar_init(bar + B_E + s, 1);
+    }
+    ptx::mbar_init(bar + B_PV, 1);
     ptx::fence_barrier_init();
   }
   // Zero the K/V rows no TMA box writes (rows_kv..127): the MMA reads up to
@@ -95,153 +115,239 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t kColS = 0, kColO = 128;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      ptx::tma_prefetch(&map_q);
-      ptx::tma_prefetch(&map_k);
-      ptx::tma_prefetch(&map_v);
-      ptx::mbar_expect_tx(bar_q, 128 * S::kRowBytes);
+    // ===================== TMA producer (whole warp, one lane issues) =====================
+    ptx::tma_prefetch(&map_q);
+    ptx::tma_prefetch(&map_k);
+    ptx::tma_prefetch(&map_v);
+    const uint32_t kv_bytes = pl.rows_kv * S::kRowBytes;
+    uint32_t kv_it = 0, ti = 0;
+    for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      TileCtx<RANK> t;
+      if (!t.init(g, pl, tile)) continue;
+      const int qb = ti & 1;
+      if (ti >= 2) ptx::mbar_wait(bar + B_QE + qb, ((ti >> 1) - 1) & 1);
+      ptx::mbar_expect_tx_w(bar + B_QF + qb, 128 * S::kRowBytes);
       for (int i = 0; i < pl.q_issues; ++i)
-        t.template load_box<RANK>(&map_q, smem + S::kQ + i * pl.q_box_x * S::kRowBytes, bar_q,
-                                  t.q_origin, i * pl.q_box_x, g);
-      const uint32_t kv_bytes = pl.rows_kv * S::kRowBytes;
-      for (int j = 0; j < nchunks; ++j) {
-        const int s = j % kStages;
-        if (j >= kStages) ptx::mbar_wait(bar_e + s, ((j / kStages) - 1) & 1);
+        t.template load_box<RANK>(&map_q, smem + S::kQ + qb * S::kTile + i * pl.q_box_x * S::kRowBytes,
+                                  bar + B_QF + qb, t.q_origin, i * pl.q_box_x, g);
+      for (int j = 0; j < t.nchunks; ++j, ++kv_it) {
+        const int s = kv_it % kStages;
+        if (kv_it >= kStages) ptx::mbar_wait(bar + B_E + s, ((kv_it / kStages) - 1) & 1);
         int org[3];
         t.chunk_origin(pl, j, org);
         uint8_t* kd = smem + S::kK + s * S::kTile;
         uint8_t* vd = smem + S::kV + s * S::kTile;
-        ptx::mbar_expect_tx(bar_k + s, kv_bytes);
+        ptx::mbar_expect_tx_w(bar + B_K + s, kv_bytes);
         for (int i = 0; i < pl.kv_issues; ++i)
-          t.template load_box<RANK>(&map_k, kd + i * pl.kv_box_x * S::kRowBytes, bar_k + s, org,
+          t.template load_box<RANK>(&map_k, kd + i * pl.kv_box_x * S::kRowBytes, bar + B_K + s, org,
                                     i * pl.kv_box_x, g);
-        ptx::mbar_expect_tx(bar_v + s, kv_bytes);
+        ptx::mbar_expect_tx_w(bar + B_V + s, kv_bytes);
         for (int i = 0; i < pl.kv_issues; ++i)
-          t.template load_box<RANK>(&map_v, vd + i * pl.kv_box_x * S::kRowBytes, bar_v + s, org,
+          t.template load_box<RANK>(&map_v, vd + i * pl.kv_box_x * S::kRowBytes, bar + B_V + s, org,
                                     i * pl.kv_box_x, g);
       }
+      ++ti;
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t kSw = D == 64 ? 2u : 4u;               // SW128 : SW64
-      constexpr uint32_t kSbo = 8 * S::kRowBytes;               // 8-row core-matrix group
-      const uint32_t idesc_s = ptx::make_idesc(128, pl.n_kv, BF16, false);
-      constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
-      const uint32_t q_addr = ptx::smem_u32(smem + S::kQ);
-      ptx::mbar_wait(bar_q, 0);
-      for (int j = 0; j < nchunks; ++j) {
-        const int s = j % kStages;
-        const uint32_t ph = (j / kStages) & 1;
-        const uint32_t k_addr = ptx::smem_u32(smem + S::kK + s * S::kTile);
-        const uint32_t v_addr = ptx::smem_u32(smem + S::kV + s * S::kTile);
-        ptx::mbar_wait(bar_k + s, ph);
-        ptx::tc_fence_after();
+    // ===================== MMA issuer (whole warp, one lane issues) =====================
+    constexpr uint32_t kSw = D == 64 ? 2u : 4u;  // SW128 : SW64
+    constexpr uint32_t kSbo = 8 * S::kRowBytes;  // 8-row core-matrix group
+    const int n1 = pl.n_kv - 64;                 // width of sub-chunk 1 (if ns == 2)
+    const uint32_t idesc_s0 = ptx::make_idesc(128, ns == 2 ? 64 : pl.n_kv, BF16, false);
+    const uint32_t idesc_s1 = ptx::make_idesc(128, ns == 2 ? n1 : 16, BF16, false);
+    constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
+    uint32_t kv_base = 0, ub = 0, ti = 0;  // chunks and sub-chunks of earlier tiles
+    for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      TileCtx<RANK> t;
+      if (!t.init(g, pl, tile)) continue;
+      const int nsub = t.nchunks * ns;
+      const int qb = ti & 1, ob = ti & 1;
+      const uint32_t q_addr = ptx::smem_u32(smem + S::kQ + qb * S::kTile);
+      auto issue_s = [&](int u) {  // u: sub-chunk index within this tile
+        const uint32_t kv = kv_base + u / ns;
+        const int h = u % ns, s = kv % kStages;
+        if (h == 0) {
+          ptx::mbar_wait(bar + B_K + s, (kv / kStages) & 1);
+          ptx::tc_fence_after();
+        }
+        const uint32_t k_addr = ptx::smem_u32(smem + S::kK + s * S::kTile) + h * 64 * S::kRowBytes;
+        const uint32_t gu = ub + u;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)  // S = Q K^T, K-dim = head_dim
-          ptx::mma_ss(tmem + kColS, ptx::make_sdesc(q_addr + kk * 32, 16, kSbo, kSw),
-                      ptx::make_sdesc(k_addr + kk * 32, 16, kSbo, kSw), idesc_s, kk > 0);
-        ptx::mma_commit(bar_s);
-        ptx::mbar_wait(bar_p, j & 1);  // softmax wrote P_j (and rescaled O)
-        ptx::mbar_wait(bar_v + s, ph);
+          ptx::mma_ss_w(tmem + (gu & 1) * 64, ptx::make_sdesc(q_addr + kk * 32, 16, kSbo, kSw),
+                        ptx::make_sdesc(k_addr + kk * 32, 16, kSbo, kSw), h ? idesc_s1 : idesc_s0,
+                        kk > 0);
+        ptx::mma_commit_w(bar + B_S + (gu & 1));
+        if (u == nsub - 1) ptx::mma_commit_w(bar + B_QE + qb);  // Q buffer reusable
+      };
+      ptx::mbar_wait(bar + B_QF + qb, (ti >> 1) & 1);
+      ptx::tc_fence_after();
+      issue_s(0);
+      if (nsub > 1) issue_s(1);
+      // O buffer ob must have been drained by the epilogue of tile ti - 2
+      if (ti >= 2) ptx::mbar_wait(bar + B_OE + ob, ((ti >> 1) - 1) & 1);
+      const uint32_t o_col = kColO + ob * D;
+      for (int u = 0; u < nsub; ++u) {
+        const uint32_t kv = kv_base + u / ns, gu = ub + u;
+        const int h = u % ns, s = kv % kStages;
+        const int width = h ? n1 : (ns == 2 ? 64 : pl.n_kv);
+        ptx::mbar_wait(bar + B_P + (gu & 1), (gu >> 1) & 1);  // softmax wrote P_u (and rescaled O)
+        if (h == 0) ptx::mbar_wait(bar + B_V + s, (kv / kStages) & 1);
         ptx::tc_fence_after();
-        for (int kk = 0; kk < pl.n_kv / 16; ++kk)  // O += P V, K-dim = keys
-          ptx::mma_ts(tmem + kColO, tmem + kColS + kk * 8,
-                      ptx::make_sdesc(v_addr + kk * 16 * S::kRowBytes, 128 * S::kRowBytes, kSbo, kSw),
-                      idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-        ptx::mma_commit(bar_e + s);  // K/V stage s free once these MMAs finish
+        const uint32_t v_addr = ptx::smem_u32(smem + S::kV + s * S::kTile) + h * 64 * S::kRowBytes;
+        for (int kk = 0; kk < width / 16; ++kk)  // O += P V, K-dim = keys
+          ptx::mma_ts_w(tmem + o_col, tmem + (gu & 1) * 64 + kk * 8,
+                        ptx::make_sdesc(v_addr + kk * 16 * S::kRowBytes, 128 * S::kRowBytes, kSbo, kSw),
+                        idesc_o, (u > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_commit_w(bar + B_PV);
+        if (h == ns - 1) ptx::mma_commit_w(bar + B_E + s);  // K/V stage free after these MMAs
+        if (u + 2 < nsub) issue_s(u + 2);
       }
-      ptx::mma_commit(bar_o);
+      ptx::mma_commit_w(bar + B_OF + ob);
+      kv_base += t.nchunks;
+      ub += nsub;
+      ++ti;
     }
   } else {
     // ===================== softmax / epilogue (128 threads) =====================
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    RowCtx<RANK> r;
-    r.init(g, pl, t, row);
     const float sl2 = g.scale_log2;
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < nchunks; ++j) {
-      uint32_t mw[4];
-      int org[3];
-      t.chunk_origin(pl, j, org);
-      r.chunk_mask(pl, org, mw);
-      ptx::mbar_wait(bar_s, j & 1);
-      ptx::tc_fence_after();
-      uint32_t sv[128];
-      NA_TMEM_LD32(trow + kColS + 0, (sv + 0));
-      NA_TMEM_LD32(trow + kColS + 32, (sv + 32));
-      NA_TMEM_LD32(trow + kColS + 64, (sv + 64));
-      NA_TMEM_LD32(trow + kColS + 96, (sv + 96));
-      ptx::tmem_ld_wait();
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        const float f = (mw[c >> 5] >> (c & 31)) & 1u ? __uint_as_float(sv[c]) * sl2 : -INFINITY;
-        sv[c] = __float_as_uint(f);
-        mx = fmaxf(mx, f);
-      }
-      // lazy rescaling: move the reference max only when it grows by > 8
-      // (factor 256); P stays <= 2^8, exact after the final normalization.
-      const bool need = mx > m_ref + 8.f;
-      if (__any_sync(0xffffffffu, need && m_ref != -INFINITY && j > 0)) {
-        const float f = need && m_ref != -INFINITY ? ptx::ex2(m_ref - mx) : 1.f;
-#pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t ov[32];
-          NA_TMEM_LD32(trow + kColO + c0, ov);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * f);
-          NA_TMEM_ST32(trow + kColO + c0, ov);
+    uint32_t ub = 0, ti = 0;
+    for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      TileCtx<RANK> t;
+      if (!t.init(g, pl, tile)) continue;
+      const int nsub = t.nchunks * ns;
+      const int ob = ti & 1;
+      const uint32_t o_col = kColO + ob * D;
+      RowCtx<RANK> r;
+      r.init(g, pl, t, row);
+      float m_ref = -INFINITY, l = 0.f;
+      uint32_t mw[4] = {0u, 0u, 0u, 0u};
+      for (int u = 0; u < nsub; ++u) {
+        const int h = u % ns;
+        const uint32_t gu = ub + u;
+        if (h == 0) {
+          int org[3];
+          t.chunk_origin(pl, u / ns, org);
+          r.chunk_mask(pl, org, mw);
         }
-        l *= f;
-      } else if (need) {
-        l *= m_ref != -INFINITY ? ptx::ex2(m_ref - mx) : 0.f;
-      }
-      if (need) m_ref = mx;
-      const float mu = m_ref == -INFINITY ? 0.f : m_ref;
-      float sum = 0.f;
+        const uint32_t w0 = h ? mw[2] : mw[0], w1 = h ? mw[3] : mw[1];
+        const uint32_t scol = (gu & 1) * 64;
+        const bool live0 = __any_sync(0xffffffffu, w0 != 0u);
+        const bool live1 = __any_sync(0xffffffffu, w1 != 0u);
+        ptx::mbar_wait(bar + B_S + (gu & 1), (gu >> 1) & 1);
+        ptx::tc_fence_after();
+        uint32_t sv[64];
+        if (live0) NA_TMEM_LD32(trow + scol, sv);
+        if (live1) NA_TMEM_LD32(trow + scol + 32, (sv + 32));
+        ptx::tmem_ld_wait();
+        // mask (only partially valid groups) and row max of the raw logits
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) {
-        const float p0 = ptx::ex2(__uint_as_float(sv[c]) - mu);
-        const float p1 = ptx::ex2(__uint_as_float(sv[c + 1]) - mu);
-        sum += p0 + p1;
-        sv[c >> 1] = pack2<BF16>(p0, p1);
+        for (int gq = 0; gq < 2; ++gq) {
+          const uint32_t w = gq ? w1 : w0;
+          const bool live = gq ? live1 : live0;
+          if (!live) continue;
+          if (!__all_sync(0xffffffffu, w == 0xffffffffu)) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              sv[32 * gq + c] = (w >> c) & 1u ? sv[32 * gq + c] : __float_as_uint(-INFINITY);
+          }
+#pragma unroll
+          for (int c = 0; c < 32; c += 8)  // independent partial maxima: short chains
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              m4[i] = fmaxf(m4[i], fmaxf(__uint_as_float(sv[32 * gq + c + i]),
+                                         __uint_as_float(sv[32 * gq + c + 4 + i])));
+        }
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        const float mx2 = mx * sl2;  // log2-domain max (-inf stays -inf)
+        // lazy rescaling: move the reference max only when it grows by > 8
+        // (factor 256); P stays <= 2^8 and the result is exact after the
+        // final normalisation.
+        const bool need = mx2 > m_ref + 8.f;
+        if (__any_sync(0xffffffffu, need && m_ref != -INFINITY)) {
+          // O must hold PV_{u-1}: S_u completing implies PV_{u-2} is done.
+          ptx::mbar_wait(bar + B_PV, (gu - 1) & 1);
+          ptx::tc_fence_after();
+          const float f = need && m_ref != -INFINITY ? ptx::ex2(m_ref - mx2) : 1.f;
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t ov[32];
+            NA_TMEM_LD32(trow + o_col + c0, ov);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * f);
+            NA_TMEM_ST32(trow + o_col + c0, ov);
+          }
+          l *= f;
+        } else if (need) {
+          l = 0.f;  // no valid key seen yet on this row
+        }
+        if (need) m_ref = mx2;
+        const float nmu = m_ref == -INFINITY ? 0.f : -m_ref;
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        uint32_t pk[32];
+#pragma unroll
+        for (int gq = 0; gq < 2; ++gq) {
+          const bool live = gq ? live1 : live0;
+          if (!live) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) pk[16 * gq + c] = 0u;
+            continue;
+          }
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            const uint32_t* s4 = sv + 32 * gq + c;
+            const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(s4[0]), __uint_as_float(s4[1])),
+                                         make_float2(sl2, sl2), make_float2(nmu, nmu));
+            const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(s4[2]), __uint_as_float(s4[3])),
+                                         make_float2(sl2, sl2), make_float2(nmu, nmu));
+            const float2 p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
+            const float2 p1 = exp2_poly2(x1);                                // FMA pipe
+            acc0 = __fadd2_rn(acc0, p0);
+            acc1 = __fadd2_rn(acc1, p1);
+            pk[16 * gq + (c >> 1)] = pack2<BF16>(p0.x, p0.y);
+            pk[16 * gq + (c >> 1) + 1] = pack2<BF16>(p1.x, p1.y);
+          }
+        }
+        l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
+        NA_TMEM_ST32(trow + scol, pk);  // P_u over the first 32 columns of its S buffer
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar + B_P + (gu & 1));
       }
-      l += sum;
-      NA_TMEM_ST32(trow + kColS + 0, (sv + 0));
-      NA_TMEM_ST32(trow + kColS + 32, (sv + 32));
-      ptx::tmem_st_wait();
+      // ---- epilogue: O / l, LSE (overlaps the next tile's S MMAs) ----
+      ptx::mbar_wait(bar + B_OF + ob, (ti >> 1) & 1);
+      ptx::tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const long long ooff = r.out_offset(g, t);
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(o_ptr) + ooff);
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t ov[32];
+        NA_TMEM_LD32(trow + o_col + c0, ov);
+        ptx::tmem_ld_wait();
+        if (r.valid) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 8)
+            dst[(c0 + c) / 8] =
+                make_uint4(pack2<BF16>(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv),
+                           pack2<BF16>(__uint_as_float(ov[c + 2]) * inv, __uint_as_float(ov[c + 3]) * inv),
+                           pack2<BF16>(__uint_as_float(ov[c + 4]) * inv, __uint_as_float(ov[c + 5]) * inv),
+                           pack2<BF16>(__uint_as_float(ov[c + 6]) * inv, __uint_as_float(ov[c + 7]) * inv));
+        }
+      }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(bar_p);
+      ptx::mbar_arrive(bar + B_OE + ob);  // O buffer may be overwritten by tile ti + 2
+      if (lse && r.valid) lse[ooff / g.D] = (m_ref + __log2f(l)) * 0.69314718055994531f;
+      ub += nsub;
+      ++ti;
     }
-    // ---- epilogue: O / l, LSE ----
-    ptx::mbar_wait(bar_o, 0);
-    ptx::tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    T* orow = reinterpret_cast<T*>(o_ptr) + r.out_offset(g, t);
-#pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      uint32_t ov[32];
-      NA_TMEM_LD32(trow + kColO + c0, ov);
-      ptx::tmem_ld_wait();
-      if (r.valid) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2)
-          pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv);
-        uint4* dst = reinterpret_cast<uint4*>(orow + c0);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      }
-    }
-    if (lse && r.valid) lse[r.out_offset(g, t) / g.D] = (m_ref + __log2f(l)) * 0.69314718055994531f;
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -262,10 +368,11 @@ cudaError_t launch(const Geom& g, const TcPlan& pl, const CUtensorMap& mq, const
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const long long grid = (long long)g.BH * pl.nres * pl.tiles;
-  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const long long tiles = (long long)g.BH * pl.nres * pl.tiles;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const unsigned grid = (unsigned)(tiles < 2LL * num_sms() ? tiles : 2LL * num_sms());
   prof_begin(KID_FWD_TC, st);
-  kern<<<(unsigned)grid, kThreads, smem, st>>>(mq, mk, mv, g, pl, o, lse);
+  kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, g, pl, o, lse, (unsigned)tiles);
   prof_end(st);
   return cudaGetLastError();
 }
@@ -300,5 +407,12 @@ cudaError_t tc_fwd(int dtype, const Geom& g, const void* q, const void* k, const
     default: return by_type<3>(dtype, g, pl, mq, mk, mv, o, lse, st);
   }
 }
+
+#ifdef NA_TRACE
+// Trace build only (libna_trace.so): point the forward kernel's event buffer.
+extern "C" int na_debug_set_trace_fwd(void* p) {
+  return cudaMemcpyToSymbol(na::g_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 }  // namespace na

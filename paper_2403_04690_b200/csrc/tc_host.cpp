@@ -134,7 +134,28 @@ TcPlan make_plan(const Geom& g, int tile_rows) {
     pl.rows_kv *= pl.ckv[a];
   }
   pl.n_kv = round16(pl.rows_kv);
+  for (int a = 0; a < 3; ++a) {
+    int s = 0;
+    while ((1 << s) < pl.tq[a]) ++s;
+    pl.tq_shift[a] = s;
+    pl.f_dil[a] = make_fastdiv(a < g.rank ? g.dil[a] : 1);
+    pl.f_ntile[a] = make_fastdiv(pl.ntile[a]);
+  }
+  pl.f_tiles = make_fastdiv(pl.tiles);
+  pl.f_nres = make_fastdiv(pl.nres);
   return pl;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
 }
 
 namespace {

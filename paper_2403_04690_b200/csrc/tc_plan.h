@@ -7,11 +7,35 @@
 // All extents are in compacted (per-residue-class) coordinates; axis 0 is
 // the outermost spatial axis, axis rank-1 the innermost (contiguous) one.
 #pragma once
+#include <stdint.h>
 
 namespace na {
 
+// Division of n < 2^31 by a runtime constant d >= 1 as a multiply-high and
+// shift (round-up method): q = (umulhi(n, mul) + n) >> shift.
+struct FastDiv {
+  uint32_t d, mul, shift;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  const uint64_t mul = (((1ull << l) - d) << 32) / d + 1;
+  return FastDiv{d, (uint32_t)mul, l};
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (__umulhi(n, f.mul) + n) >> f.shift;
+}
+__device__ __forceinline__ uint32_t fmod_(uint32_t n, uint32_t q, const FastDiv& f) {
+  return n - q * f.d;
+}
+#endif
+
 struct TcPlan {
-  int tq[3];       // query tile extent per axis (product 128; 1 beyond rank)
+  int tq[3];       // query tile extent per axis (power of two, product 128; 1 beyond rank)
+  int tq_shift[3]; // log2(tq)
   int ckv[3];      // KV chunk box extent per axis (product <= 128)
   int ntile[3];    // tiles per axis over the largest residue class
   int tiles;       // prod(ntile)
@@ -22,6 +46,7 @@ struct TcPlan {
   int kv_issues;   // TMA issues per K or V chunk
   int q_box_x;     // compacted x extent per Q issue
   int kv_box_x;    // compacted x extent per KV issue
+  FastDiv f_tiles, f_nres, f_dil[3], f_ntile[3];
 };
 
 }  // namespace na
