@@ -6,7 +6,7 @@
 //   dP = PN(dO, V)          dS = P o (dP - D),  D_x = <dO_x, O_x>
 //   dQ = scale NN(dS, K)    dK = scale IN(dS, Q)    dV = IN(P, dO)
 // Two kernels, each output element has exactly one writer (no atomics):
-//   fna_dkdv_tc  key-stationary: a CTA owns 128 keys of one residue class and
+//   fna_dkdv_tc  key-stationary: a tile = 128 keys of one residue class; it
 //                streams the query chunks of the tile's INVERSE halo
 //                [inv_start(y_lo), inv_end(y_hi)] (the IN gather pattern,
 //                P:253-258).  Per 64-query sub-chunk: S^T = K Q^T and
@@ -15,12 +15,15 @@
 //                TMEM as 16-bit), then dV += P^T dO and dK += dS^T Q (TS MMAs).
 //   fna_dq_tc    query-stationary over the forward halo: S = Q K^T, dP = dO V^T,
 //                dS = P (dP - D), dQ += dS K.
-// Warp roles (320 threads, 1 CTA per SM): warp 0 TMA producer, warp 1 TMEM
-// owner + single-thread MMA issuer, warps 2..9 two compute warpgroups
-// (thread = TMEM lane = stationary row).  Sub-chunk u lives in TMEM buffer
-// u%2 and is processed by warpgroup u%2, so the tensor core computes
-// sub-chunk u+1 while warpgroup u%2 works on u (ping-pong):
-//   MMA order: ST_0, ST_1, [P_0] OUT_0, ST_2, [P_1] OUT_1, ST_3, ...
+// Persistent, 1 CTA per SM walking tiles blockIdx.x, +gridDim.x, ...
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA
+// issuer (whole warps, one elected lane issues), warps 2..9 two compute
+// warpgroups (thread = TMEM lane = stationary row).  Sub-chunk with global
+// index gu lives in TMEM buffer gu%2 and is processed by warpgroup gu%2, so
+// the tensor core computes the next sub-chunk while a warpgroup works:
+//   MMA order per tile: ST_0, ST_1, [P_0] OUT_0, ST_2, [P_1] OUT_1, ST_3, ...
+// Stationary tiles are double-buffered in smem and the output accumulators
+// in TMEM, so tile i+1's loads and MMAs overlap tile i's epilogue.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -34,35 +37,45 @@
 namespace na {
 namespace {
 
+#ifdef NA_TRACE
+static __device__ int g_trace_sel;  // trace build: 1 = dK/dV kernel, 0 = dQ kernel
+#define NA_BWD_TRACE_ON (g_trace_sel == (KV_STATIONARY ? 1 : 0))
+#else
+#define NA_BWD_TRACE_ON false
+#endif
+
 constexpr int kStages = 2;
 constexpr int kThreads = 320;
+constexpr int kCompute = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
 struct BwdSmem {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTile = 128 * kRowBytes;
-  static constexpr int kA0 = 0;                       // stationary tile 0 (K | Q)
-  static constexpr int kA1 = kA0 + kTile;             // stationary tile 1 (V | dO)
-  static constexpr int kB0 = kA1 + kTile;             // streamed [kStages] (Q | K)
+  static constexpr int kA = 0;                        // stationary [2 bufs][2 tiles] (K,V | Q,dO)
+  static constexpr int kB0 = kA + 4 * kTile;          // streamed [kStages] (Q | K)
   static constexpr int kB1 = kB0 + kStages * kTile;   // streamed [kStages] (dO | V)
-  static constexpr int kVec = kB1 + kStages * kTile;  // [group][slot][LSE2 x64 | D x64] fp32
+  static constexpr int kVec = kB1 + kStages * kTile;  // [parity][slot][LSE2 x64 | D x64] fp32
   static constexpr int kBar = kVec + 2 * 2 * 128 * 4;
   static constexpr int kBytes = kBar + 256;
 };
 
 // TMEM columns: [0,128) two 64-column S-like buffers, [128,256) two dP-like
-// buffers, [256, 256+D) first output, [256+D, 256+2D) second output.
+// buffers, [256 + 128*ob, ...) output accumulators of tile parity ob
+// (first output at +0, second at +D).
 constexpr uint32_t kColS = 0, kColP = 128, kColOut = 256;
 
 enum : int {
-  B_A = 0,                  // stationary tiles loaded
-  B_B = 1,                  // streamed stage full [kStages]
+  B_AF = 0,                 // stationary tiles full [2]
+  B_AE = B_AF + 2,          // stationary tiles empty [2]
+  B_B = B_AE + 2,           // streamed stage full [kStages]
   B_E = B_B + kStages,      // streamed stage empty [kStages]
   B_S = B_E + kStages,      // S and dP of a sub-chunk ready [2]
   B_P = B_S + 2,            // packed operands of a sub-chunk written [2] (128 arrivals)
-  B_O = B_P + 2,            // outputs final
-  B_COUNT = B_O + 1
+  B_OF = B_P + 2,           // outputs of a tile final [2]
+  B_OE = B_OF + 2,          // outputs drained by the epilogue [2] (256 arrivals)
+  B_COUNT = B_OE + 2
 };
 
 template <int RANK, int D, bool BF16, bool KV_STATIONARY>
@@ -70,7 +83,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
                                          const CUtensorMap& map_b0, const CUtensorMap& map_b1,
                                          const Geom& g, const TcPlan& pl, const float* __restrict__ lse,
                                          const float* __restrict__ dvec, void* __restrict__ out0,
-                                         void* __restrict__ out1) {
+                                         void* __restrict__ out1, unsigned num_tiles) {
   using S = BwdSmem<D>;
   using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -78,25 +91,22 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + B_COUNT);
   float* vec = reinterpret_cast<float*>(smem + S::kVec);
-
-  TileCtx<RANK> t;
-  if (!t.init(g, pl, blockIdx.x, /*inverse=*/KV_STATIONARY)) return;
-  const int nchunks = t.nchunks;
   const int ns = pl.n_kv > 64 ? 2 : 1;
-  const int nsub = nchunks * ns;
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(bar + B_A, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(bar + B_AF + b, 1);
+      ptx::mbar_init(bar + B_AE + b, 1);
+      ptx::mbar_init(bar + B_S + b, 1);
+      ptx::mbar_init(bar + B_P + b, 128);
+      ptx::mbar_init(bar + B_OF + b, 1);
+      ptx::mbar_init(bar + B_OE + b, kCompute);
+    }
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(bar + B_B + s, 1);
       ptx::mbar_init(bar + B_E + s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(bar + B_S + b, 1);
-      ptx::mbar_init(bar + B_P + b, 128);
-    }
-    ptx::mbar_init(bar + B_O, 1);
     ptx::fence_barrier_init();
   }
   if (pl.rows_kv < 128) {  // rows no TMA box writes must be finite (zero)
@@ -116,22 +126,29 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
 
   if (warp == 0) {
     // ===================== TMA producer (whole warp, one lane issues) =====================
-    {
-      ptx::tma_prefetch(&map_a0);
-      ptx::tma_prefetch(&map_a1);
-      ptx::tma_prefetch(&map_b0);
-      ptx::tma_prefetch(&map_b1);
-      ptx::mbar_expect_tx_w(bar + B_A, 2 * 128 * S::kRowBytes);
+    ptx::tma_prefetch(&map_a0);
+    ptx::tma_prefetch(&map_a1);
+    ptx::tma_prefetch(&map_b0);
+    ptx::tma_prefetch(&map_b1);
+    const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes;
+    uint32_t kv_it = 0, ti = 0;
+    for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      TileCtx<RANK> t;
+      if (!t.init(g, pl, tile, /*inverse=*/KV_STATIONARY)) continue;
+      const int ab = ti & 1;
+      if (ti >= 2) ptx::mbar_wait(bar + B_AE + ab, ((ti >> 1) - 1) & 1);
+      uint8_t* a0 = smem + S::kA + (2 * ab) * S::kTile;
+      uint8_t* a1 = a0 + S::kTile;
+      ptx::mbar_expect_tx_w(bar + B_AF + ab, 2 * 128 * S::kRowBytes);
       for (int i = 0; i < pl.q_issues; ++i) {
-        t.template load_box<RANK>(&map_a0, smem + S::kA0 + i * pl.q_box_x * S::kRowBytes, bar + B_A,
+        t.template load_box<RANK>(&map_a0, a0 + i * pl.q_box_x * S::kRowBytes, bar + B_AF + ab,
                                   t.q_origin, i * pl.q_box_x, g);
-        t.template load_box<RANK>(&map_a1, smem + S::kA1 + i * pl.q_box_x * S::kRowBytes, bar + B_A,
+        t.template load_box<RANK>(&map_a1, a1 + i * pl.q_box_x * S::kRowBytes, bar + B_AF + ab,
                                   t.q_origin, i * pl.q_box_x, g);
       }
-      const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes;
-      for (int j = 0; j < nchunks; ++j) {
-        const int s = j % kStages;
-        if (j >= kStages) ptx::mbar_wait(bar + B_E + s, ((j / kStages) - 1) & 1);
+      for (int j = 0; j < t.nchunks; ++j, ++kv_it) {
+        const int s = kv_it % kStages;
+        if (kv_it >= kStages) ptx::mbar_wait(bar + B_E + s, ((kv_it / kStages) - 1) & 1);
         int org[3];
         t.chunk_origin(pl, j, org);
         ptx::mbar_expect_tx_w(bar + B_B + s, bytes);
@@ -142,203 +159,253 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
                                     bar + B_B + s, org, i * pl.kv_box_x, g);
         }
       }
+      ++ti;
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (whole warp, one lane issues) =====================
-    {
-      constexpr uint32_t kSw = D == 64 ? 2u : 4u;
-      constexpr uint32_t kSbo = 8 * S::kRowBytes;
-      const int n1 = pl.n_kv - 64;
-      const uint32_t idesc_s0 = ptx::make_idesc(128, ns == 2 ? 64 : pl.n_kv, BF16, false);
-      const uint32_t idesc_s1 = ptx::make_idesc(128, ns == 2 ? n1 : 16, BF16, false);
-      constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
-      const uint32_t a0 = ptx::smem_u32(smem + S::kA0), a1 = ptx::smem_u32(smem + S::kA1);
+    constexpr uint32_t kSw = D == 64 ? 2u : 4u;
+    constexpr uint32_t kSbo = 8 * S::kRowBytes;
+    const int n1 = pl.n_kv - 64;
+    const uint32_t idesc_s0 = ptx::make_idesc(128, ns == 2 ? 64 : pl.n_kv, BF16, false);
+    const uint32_t idesc_s1 = ptx::make_idesc(128, ns == 2 ? n1 : 16, BF16, false);
+    constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
+    uint32_t kv_base = 0, ub = 0, ti = 0;
+    int tr = 0;
+    (void)tr;
+    for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      TileCtx<RANK> t;
+      if (!t.init(g, pl, tile, /*inverse=*/KV_STATIONARY)) continue;
+      const int nsub = t.nchunks * ns;
+      const int ab = ti & 1, ob = ti & 1;
+      const uint32_t a0 = ptx::smem_u32(smem + S::kA + (2 * ab) * S::kTile);
+      const uint32_t a1 = a0 + S::kTile;
+      const uint32_t out = kColOut + ob * 128;
       auto issue_st = [&](int u) {
-        const int j = u / ns, h = u % ns, s = j % kStages;
+        const uint32_t kv = kv_base + u / ns, gu = ub + u;
+        const int h = u % ns, s = kv % kStages;
         if (h == 0) {
-          ptx::mbar_wait(bar + B_B + s, (j / kStages) & 1);
+          ptx::mbar_wait(bar + B_B + s, (kv / kStages) & 1);
           ptx::tc_fence_after();
         }
         const uint32_t off = h * 64 * S::kRowBytes;
         const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
         const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
         const uint32_t id = h ? idesc_s1 : idesc_s0;
-        const uint32_t buf = (u & 1) * 64;
+        const uint32_t buf = (gu & 1) * 64;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
           ptx::mma_ss_w(tmem + kColS + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
-                      ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
+                        ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
           ptx::mma_ss_w(tmem + kColP + buf, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
-                      ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
+                        ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
         }
-        ptx::mma_commit_w(bar + B_S + (u & 1));
+        ptx::mma_commit_w(bar + B_S + (gu & 1));
+        if (u == nsub - 1) ptx::mma_commit_w(bar + B_AE + ab);  // stationary tiles reusable
       };
-      ptx::mbar_wait(bar + B_A, 0);
+      ptx::mbar_wait(bar + B_AF + ab, (ti >> 1) & 1);
+      ptx::tc_fence_after();
       issue_st(0);
       if (nsub > 1) issue_st(1);
+      if (ti >= 2) ptx::mbar_wait(bar + B_OE + ob, ((ti >> 1) - 1) & 1);  // outputs drained
       for (int u = 0; u < nsub; ++u) {
-        const int j = u / ns, h = u % ns, s = j % kStages;
+        const uint32_t kv = kv_base + u / ns, gu = ub + u;
+        const int h = u % ns, s = kv % kStages;
         const int width = h ? n1 : (ns == 2 ? 64 : pl.n_kv);
         const uint32_t off = h * 64 * S::kRowBytes;
         const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
         const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
-        const uint32_t buf = (u & 1) * 64;
-        ptx::mbar_wait(bar + B_P + (u & 1), (u >> 1) & 1);
+        const uint32_t buf = (gu & 1) * 64;
+        ptx::mbar_wait(bar + B_P + (gu & 1), (gu >> 1) & 1);
+        if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 11);
         ptx::tc_fence_after();
         for (int kk = 0; kk < width / 16; ++kk) {
           const uint32_t boff = kk * 16 * S::kRowBytes;
           const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
           if constexpr (KV_STATIONARY) {
             // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
-            ptx::mma_ts_w(tmem + kColOut + D, tmem + kColS + buf + kk * 8,
-                        ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
-            ptx::mma_ts_w(tmem + kColOut, tmem + kColP + buf + kk * 8,
-                        ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+            ptx::mma_ts_w(tmem + out + D, tmem + kColS + buf + kk * 8,
+                          ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+            ptx::mma_ts_w(tmem + out, tmem + kColP + buf + kk * 8,
+                          ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
           } else {
             // dQ += dS K
-            ptx::mma_ts_w(tmem + kColOut, tmem + kColS + buf + kk * 8,
-                        ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+            ptx::mma_ts_w(tmem + out, tmem + kColS + buf + kk * 8,
+                          ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
           }
         }
         if (h == ns - 1) ptx::mma_commit_w(bar + B_E + s);
+        if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 12);
         if (u + 2 < nsub) issue_st(u + 2);
       }
-      ptx::mma_commit_w(bar + B_O);
+      ptx::mma_commit_w(bar + B_OF + ob);
+      kv_base += t.nchunks;
+      ub += nsub;
+      ++ti;
     }
   } else {
     // ===================== compute warpgroups (2 x 128 threads) =====================
-    const int grp = (warp - 2) >> 2;     // processes sub-chunks u with u % 2 == grp
+    const int grp = (warp - 2) >> 2;     // processes sub-chunks with gu % 2 == grp
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const int gtid = ((warp - 2) & 3) * 32 + lane;  // 0..127 within the group
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    RowCtx<RANK> r;
-    r.init(g, pl, t, row, /*inverse=*/KV_STATIONARY);
     const float sl2 = g.scale_log2;
-    float row_lse2 = 0.f, row_d = 0.f;
-    if constexpr (!KV_STATIONARY) {
-      if (r.valid) {
-        const long long tok = r.out_offset(g, t) / g.D;
-        row_lse2 = lse[tok] * kLog2e;
-        row_d = dvec[tok];
+    uint32_t ub = 0, ti = 0, it = 0;
+    int tr = 0;
+    (void)tr;
+    const bool tracer = NA_BWD_TRACE_ON && lane == 0 && (warp == 2 || warp == 6);
+    for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      TileCtx<RANK> t;
+      if (!t.init(g, pl, tile, /*inverse=*/KV_STATIONARY)) continue;
+      const int nsub = t.nchunks * ns;
+      const int ob = ti & 1;
+      RowCtx<RANK> r;
+      r.init(g, pl, t, row, /*inverse=*/KV_STATIONARY);
+      float row_lse2 = 0.f, row_d = 0.f;
+      if constexpr (!KV_STATIONARY) {
+        if (r.valid) {
+          const long long tok = r.out_offset(g, t) / g.D;
+          row_lse2 = lse[tok] * kLog2e;
+          row_d = dvec[tok];
+        }
       }
-    }
-    uint32_t mw[4] = {0u, 0u, 0u, 0u};
-    int it = 0;
-    for (int u = grp; u < nsub; u += 2, ++it) {
-      const int j = u / ns, h = u % ns;
-      int org[3];
-      t.chunk_origin(pl, j, org);
-      r.chunk_mask(pl, org, mw);
-      const uint32_t w0 = h ? mw[2] : mw[0], w1 = h ? mw[3] : mw[1];
-      float* cv = vec + (grp * 2 + (it & 1)) * 128;  // [LSE2 x64 | D x64] of this sub-chunk's columns
-      if constexpr (KV_STATIONARY) {
-        // stage the partner (query) LSE and D values of this sub-chunk's columns
-        const int col = gtid & 63, which = gtid >> 6;
-        const int ccol = h * 64 + col;  // column within the chunk
-        float val = 0.f;
-        if (ccol < pl.rows_kv) {
-          int rem = ccol;
-          bool ok = true;
-          long long tok = 0;
+      uint32_t mw[4] = {0u, 0u, 0u, 0u};
+      for (int u = (int)((grp - ub) & 1u); u < nsub; u += 2, ++it) {
+        const uint32_t gu = ub + u;
+        const int j = u / ns, h = u % ns;
+        int org[3];
+        t.chunk_origin(pl, j, org);
+        r.chunk_mask(pl, org, mw);
+        const uint32_t w0 = h ? mw[2] : mw[0], w1 = h ? mw[3] : mw[1];
+        float* cv = vec + (grp * 2 + (it & 1)) * 128;  // [LSE2 x64 | D x64] of this sub-chunk's columns
+        if constexpr (KV_STATIONARY) {
+          // stage the partner (query) LSE and D values of this sub-chunk's columns
+          const int col = gtid & 63, which = gtid >> 6;
+          const int ccol = h * 64 + col;  // column within the chunk
+          float val = 0.f;
+          if (ccol < pl.rows_kv) {
+            int rem = ccol;
+            bool ok = true;
+            long long tok = 0;
 #pragma unroll
-          for (int a = 2; a >= 0; --a) {
-            if (a >= RANK) continue;
-            const int cc = org[a] + rem % pl.ckv[a];
-            rem /= pl.ckv[a];
-            ok = ok && cc < t.Lr[a];
-            tok += (long long)(t.r[a] + g.dil[a] * cc) * g.tstride[a];
+            for (int a = 2; a >= 0; --a) {
+              if (a >= RANK) continue;
+              const int cc = org[a] + (a == 0 ? rem : rem % pl.ckv[a]);
+              if (a > 0) rem /= pl.ckv[a];
+              ok = ok && cc < t.Lr[a];
+              tok += (long long)(t.r[a] + g.dil[a] * cc) * g.tstride[a];
+            }
+            if (ok) {
+              tok += (long long)t.bh * g.N;
+              val = which == 0 ? lse[tok] * kLog2e : dvec[tok];
+            }
           }
-          if (ok) {
-            tok += (long long)t.bh * g.N;
-            val = which == 0 ? lse[tok] * kLog2e : dvec[tok];
+          cv[which * 64 + col] = val;
+          ptx::named_bar_sync(1 + grp, 128);
+        }
+        const uint32_t buf = (gu & 1) * 64;
+        if (tracer) NA_TRACE_EV(2 + grp, tr, 19);
+        ptx::mbar_wait(bar + B_S + (gu & 1), (gu >> 1) & 1);
+        if (tracer) NA_TRACE_EV(2 + grp, tr, 20);
+        ptx::tc_fence_after();
+        uint32_t pk_p[32], pk_s[32];
+#pragma unroll
+        for (int gq = 0; gq < 2; ++gq) {
+          const uint32_t w = gq ? w1 : w0;
+          if (!__any_sync(0xffffffffu, w != 0u)) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) pk_p[16 * gq + c] = pk_s[16 * gq + c] = 0u;
+            continue;
+          }
+          const bool full = __all_sync(0xffffffffu, w == 0xffffffffu);
+          uint32_t sv[32], pv[32];
+          NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
+          NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            float4 nl4, dd4;
+            if constexpr (KV_STATIONARY) {
+              nl4 = *reinterpret_cast<const float4*>(cv + 32 * gq + c);
+              dd4 = *reinterpret_cast<const float4*>(cv + 64 + 32 * gq + c);
+              nl4 = make_float4(-nl4.x, -nl4.y, -nl4.z, -nl4.w);
+            } else {
+              nl4 = make_float4(-row_lse2, -row_lse2, -row_lse2, -row_lse2);
+              dd4 = make_float4(row_d, row_d, row_d, row_d);
+            }
+            float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])),
+                                   make_float2(sl2, sl2), make_float2(nl4.x, nl4.y));
+            float2 x1 = __ffma2_rn(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])),
+                                   make_float2(sl2, sl2), make_float2(nl4.z, nl4.w));
+            if (!full) {
+              x0.x = (w >> c) & 1u ? x0.x : -INFINITY;
+              x0.y = (w >> (c + 1)) & 1u ? x0.y : -INFINITY;
+              x1.x = (w >> (c + 2)) & 1u ? x1.x : -INFINITY;
+              x1.y = (w >> (c + 3)) & 1u ? x1.y : -INFINITY;
+            }
+            const float2 p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
+            const float2 p1 = exp2_poly2(x1);                                // FMA pipe
+            const float2 ds0 = __fmul2_rn(p0, __fadd2_rn(make_float2(__uint_as_float(pv[c]),
+                                                                     __uint_as_float(pv[c + 1])),
+                                                         make_float2(-dd4.x, -dd4.y)));
+            const float2 ds1 = __fmul2_rn(p1, __fadd2_rn(make_float2(__uint_as_float(pv[c + 2]),
+                                                                     __uint_as_float(pv[c + 3])),
+                                                         make_float2(-dd4.z, -dd4.w)));
+            pk_p[16 * gq + (c >> 1)] = pack2<BF16>(p0.x, p0.y);
+            pk_p[16 * gq + (c >> 1) + 1] = pack2<BF16>(p1.x, p1.y);
+            pk_s[16 * gq + (c >> 1)] = pack2<BF16>(ds0.x, ds0.y);
+            pk_s[16 * gq + (c >> 1) + 1] = pack2<BF16>(ds1.x, ds1.y);
           }
         }
-        cv[which * 64 + col] = val;
-        ptx::named_bar_sync(1 + grp, 128);
+        if constexpr (KV_STATIONARY) {
+          NA_TMEM_ST32(trow + kColS + buf, pk_p);  // P^T  -> A of dV += P^T dO
+          NA_TMEM_ST32(trow + kColP + buf, pk_s);  // dS^T -> A of dK += dS^T Q
+        } else {
+          NA_TMEM_ST32(trow + kColS + buf, pk_s);  // dS -> A of dQ += dS K
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar + B_P + (gu & 1));
+        if (tracer) NA_TRACE_EV(2 + grp, tr, 21);
       }
-      const uint32_t buf = (u & 1) * 64;
-      ptx::mbar_wait(bar + B_S + (u & 1), (u >> 1) & 1);
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 22);
+      // ---- epilogue (overlaps the next tile's MMAs) ----
+      ptx::mbar_wait(bar + B_OF + ob, (ti >> 1) & 1);
       ptx::tc_fence_after();
-      uint32_t pk_p[32], pk_s[32];
+      // KV-stationary: group 0 writes dK (x scale), group 1 writes dV.
+      // Q-stationary: the two groups split dQ's D columns.
+      const long long off = r.out_offset(g, t);
+      constexpr int kCols = KV_STATIONARY ? D : D / 2;
+      const uint32_t src = kColOut + ob * 128 + (KV_STATIONARY ? grp * D : grp * (D / 2));
+      T* dst = reinterpret_cast<T*>(KV_STATIONARY && grp ? out1 : out0) + off +
+               (KV_STATIONARY ? 0 : grp * (D / 2));
+      const float mul = (KV_STATIONARY && grp) ? 1.f : g.scale;
 #pragma unroll
-      for (int gq = 0; gq < 2; ++gq) {
-        const uint32_t w = gq ? w1 : w0;
-        if (!__any_sync(0xffffffffu, w != 0u)) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) pk_p[16 * gq + c] = pk_s[16 * gq + c] = 0u;
-          continue;
-        }
-        const bool full = __all_sync(0xffffffffu, w == 0xffffffffu);
-        uint32_t sv[32], pv[32];
-        NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
-        NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
+      for (int c0 = 0; c0 < kCols; c0 += 16) {
+        uint32_t ov[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3]), "=r"(ov[4]), "=r"(ov[5]), "=r"(ov[6]),
+              "=r"(ov[7]), "=r"(ov[8]), "=r"(ov[9]), "=r"(ov[10]), "=r"(ov[11]), "=r"(ov[12]),
+              "=r"(ov[13]), "=r"(ov[14]), "=r"(ov[15])
+            : "r"(trow + src + c0));
         ptx::tmem_ld_wait();
+        if (r.valid) {
+          uint32_t pk[8];
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          float2 nl, dd;
-          if constexpr (KV_STATIONARY) {
-            nl = make_float2(-cv[32 * gq + c], -cv[32 * gq + c + 1]);
-            dd = make_float2(cv[64 + 32 * gq + c], cv[64 + 32 * gq + c + 1]);
-          } else {
-            nl = make_float2(-row_lse2, -row_lse2);
-            dd = make_float2(row_d, row_d);
-          }
-          float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])),
-                                make_float2(sl2, sl2), nl);
-          if (!full) {
-            x.x = (w >> c) & 1u ? x.x : -INFINITY;
-            x.y = (w >> (c + 1)) & 1u ? x.y : -INFINITY;
-          }
-          const float2 p = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
-          const float2 ds = __fmul2_rn(p, __fadd2_rn(make_float2(__uint_as_float(pv[c]),
-                                                                 __uint_as_float(pv[c + 1])),
-                                                     make_float2(-dd.x, -dd.y)));
-          pk_p[16 * gq + (c >> 1)] = pack2<BF16>(p.x, p.y);
-          pk_s[16 * gq + (c >> 1)] = pack2<BF16>(ds.x, ds.y);
+          for (int c = 0; c < 16; c += 2)
+            pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+          d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
       }
-      if constexpr (KV_STATIONARY) {
-        NA_TMEM_ST32(trow + kColS + buf, pk_p);  // P^T  -> A of dV += P^T dO
-        NA_TMEM_ST32(trow + kColP + buf, pk_s);  // dS^T -> A of dK += dS^T Q
-      } else {
-        NA_TMEM_ST32(trow + kColS + buf, pk_s);  // dS -> A of dQ += dS K
-      }
-      ptx::tmem_st_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(bar + B_P + (u & 1));
-    }
-    // ---- epilogue ----
-    ptx::mbar_wait(bar + B_O, 0);
-    ptx::tc_fence_after();
-    // KV-stationary: group 0 writes dK (x scale), group 1 writes dV.
-    // Q-stationary: the two groups split dQ's D columns.
-    const long long off = r.out_offset(g, t);
-    constexpr int kCols = KV_STATIONARY ? D : D / 2;
-    const uint32_t src = KV_STATIONARY ? kColOut + grp * D : kColOut + grp * (D / 2);
-    T* dst = reinterpret_cast<T*>(KV_STATIONARY && grp ? out1 : out0) + off +
-             (KV_STATIONARY ? 0 : grp * (D / 2));
-    const float mul = (KV_STATIONARY && grp) ? 1.f : g.scale;
-#pragma unroll
-    for (int c0 = 0; c0 < kCols; c0 += 16) {
-      uint32_t ov[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3]), "=r"(ov[4]), "=r"(ov[5]), "=r"(ov[6]),
-            "=r"(ov[7]), "=r"(ov[8]), "=r"(ov[9]), "=r"(ov[10]), "=r"(ov[11]), "=r"(ov[12]),
-            "=r"(ov[13]), "=r"(ov[14]), "=r"(ov[15])
-          : "r"(trow + src + c0));
-      ptx::tmem_ld_wait();
-      if (r.valid) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int c = 0; c < 16; c += 2)
-          pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
-        d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
+      ptx::mbar_arrive(bar + B_OE + ob);
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 23);
+      ub += nsub;
+      ++ti;
     }
   }
   ptx::tc_fence_before();
@@ -355,8 +422,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fna_dkdv_tc(const __grid_constant__ CUtensorMap map_k, const __grid_constant__ CUtensorMap map_v,
                 const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_do,
                 Geom g, TcPlan pl, const float* __restrict__ lse, const float* __restrict__ dvec,
-                void* __restrict__ dk, void* __restrict__ dv) {
-  bwd_body<RANK, D, BF16, true>(map_k, map_v, map_q, map_do, g, pl, lse, dvec, dk, dv);
+                void* __restrict__ dk, void* __restrict__ dv, unsigned num_tiles) {
+  bwd_body<RANK, D, BF16, true>(map_k, map_v, map_q, map_do, g, pl, lse, dvec, dk, dv, num_tiles);
 }
 
 // dQ: query-stationary over the forward halo.
@@ -365,8 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fna_dq_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_do,
               const __grid_constant__ CUtensorMap map_k, const __grid_constant__ CUtensorMap map_v,
               Geom g, TcPlan pl, const float* __restrict__ lse, const float* __restrict__ dvec,
-              void* __restrict__ dq) {
-  bwd_body<RANK, D, BF16, false>(map_q, map_do, map_k, map_v, g, pl, lse, dvec, dq, nullptr);
+              void* __restrict__ dq, unsigned num_tiles) {
+  bwd_body<RANK, D, BF16, false>(map_q, map_do, map_k, map_v, g, pl, lse, dvec, dq, nullptr, num_tiles);
 }
 
 template <int RANK, int D, bool BF16>
@@ -385,15 +452,16 @@ cudaError_t launch_both(const Geom& g, const TcPlan& pl, const CUtensorMap* m, c
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const long long grid = (long long)g.BH * pl.nres * pl.tiles;
-  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const long long tiles = (long long)g.BH * pl.nres * pl.tiles;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const unsigned grid = (unsigned)(tiles < num_sms() ? tiles : num_sms());
   prof_begin(KID_DKDV_TC, st);
-  kdkdv<<<(unsigned)grid, kThreads, smem, st>>>(m[1], m[2], m[4], m[7], g, pl, lse, dvec, dk, dv);
+  kdkdv<<<grid, kThreads, smem, st>>>(m[1], m[2], m[4], m[7], g, pl, lse, dvec, dk, dv, (unsigned)tiles);
   prof_end(st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   prof_begin(KID_DQ_TC, st);
-  kdq<<<(unsigned)grid, kThreads, smem, st>>>(m[0], m[3], m[5], m[6], g, pl, lse, dvec, dq);
+  kdq<<<grid, kThreads, smem, st>>>(m[0], m[3], m[5], m[6], g, pl, lse, dvec, dq, (unsigned)tiles);
   prof_end(st);
   return cudaGetLastError();
 }
@@ -435,3 +503,11 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
 }
 
 }  // namespace na
+
+#ifdef NA_TRACE
+// Trace build only (libna_trace.so): point the backward kernels' event buffer.
+extern "C" int na_debug_set_trace_bwd(void* p, int which) {
+  if (cudaMemcpyToSymbol(na::g_trace_sel, &which, sizeof(which)) != cudaSuccess) return 1;
+  return cudaMemcpyToSymbol(na::g_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 1;
+}
+#endif
