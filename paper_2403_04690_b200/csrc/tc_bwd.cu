@@ -46,7 +46,11 @@ static __device__ int g_trace_sel;  // trace build: 1 = dK/dV kernel, 0 = dQ ker
 
 constexpr int kStages = 2;
 constexpr int kThreads = 320;
-constexpr int kCompute = 256;
+constexpr int kCompute = 256;  // compute threads (warps 0..7)
+// The warp scheduler favours the highest warp id among eligible warps, so the
+// latency-critical single-lane roles take the highest ids.
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
@@ -118,13 +122,13 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
     }
     ptx::fence_proxy_async();
   }
-  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaWarp) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == kProducerWarp) {
     // ===================== TMA producer (whole warp, one lane issues) =====================
     ptx::tma_prefetch(&map_a0);
     ptx::tma_prefetch(&map_a1);
@@ -161,7 +165,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
       }
       ++ti;
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (whole warp, one lane issues) =====================
     constexpr uint32_t kSw = D == 64 ? 2u : 4u;
     constexpr uint32_t kSbo = 8 * S::kRowBytes;
@@ -245,16 +249,16 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
     }
   } else {
     // ===================== compute warpgroups (2 x 128 threads) =====================
-    const int grp = (warp - 2) >> 2;     // processes sub-chunks with gu % 2 == grp
+    const int grp = warp >> 2;           // processes sub-chunks with gu % 2 == grp
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
-    const int gtid = ((warp - 2) & 3) * 32 + lane;  // 0..127 within the group
+    const int gtid = (warp & 3) * 32 + lane;  // 0..127 within the group
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = g.scale_log2;
     uint32_t ub = 0, ti = 0, it = 0;
     int tr = 0;
     (void)tr;
-    const bool tracer = NA_BWD_TRACE_ON && lane == 0 && (warp == 2 || warp == 6);
+    const bool tracer = NA_BWD_TRACE_ON && lane == 0 && (warp == 0 || warp == 4);
     for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       TileCtx<RANK> t;
       if (!t.init(g, pl, tile, /*inverse=*/KV_STATIONARY)) continue;
@@ -271,7 +275,43 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
         }
       }
       uint32_t mw[4] = {0u, 0u, 0u, 0u};
-      for (int u = (int)((grp - ub) & 1u); u < nsub; u += 2, ++it) {
+      // Partner (query) LSE / D values of a sub-chunk's 64 columns, staged in
+      // smem: thread gtid fetches column gtid & 63 of LSE (gtid < 64) or D.
+      // The fetch for the group's NEXT sub-chunk is issued before computing
+      // the current one, so its global-load latency overlaps that work.
+      auto fetch = [&](int uu) -> float {
+        const int col = gtid & 63, which = gtid >> 6;
+        const int ccol = (uu % ns) * 64 + col;  // column within the chunk
+        float val = 0.f;
+        if (ccol < pl.rows_kv) {
+          int org[3];
+          t.chunk_origin(pl, uu / ns, org);
+          int rem = ccol;
+          bool ok = true;
+          long long tok = 0;
+#pragma unroll
+          for (int a = 2; a >= 0; --a) {
+            if (a >= RANK) continue;
+            const int cc = org[a] + (a == 0 ? rem : rem % pl.ckv[a]);
+            if (a > 0) rem /= pl.ckv[a];
+            ok = ok && cc < t.Lr[a];
+            tok += (long long)(t.r[a] + g.dil[a] * cc) * g.tstride[a];
+          }
+          if (ok) {
+            tok += (long long)t.bh * g.N;
+            val = which == 0 ? lse[tok] * kLog2e : dvec[tok];
+          }
+        }
+        return val;
+      };
+      const int u_first = (int)((grp - ub) & 1u);
+      if constexpr (KV_STATIONARY) {
+        if (u_first < nsub) {
+          vec[(grp * 2 + (it & 1)) * 128 + (gtid >> 6) * 64 + (gtid & 63)] = fetch(u_first);
+          ptx::named_bar_sync(1 + grp, 128);
+        }
+      }
+      for (int u = u_first; u < nsub; u += 2, ++it) {
         const uint32_t gu = ub + u;
         const int j = u / ns, h = u % ns;
         int org[3];
@@ -279,30 +319,9 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
         r.chunk_mask(pl, org, mw);
         const uint32_t w0 = h ? mw[2] : mw[0], w1 = h ? mw[3] : mw[1];
         float* cv = vec + (grp * 2 + (it & 1)) * 128;  // [LSE2 x64 | D x64] of this sub-chunk's columns
+        float next_val = 0.f;
         if constexpr (KV_STATIONARY) {
-          // stage the partner (query) LSE and D values of this sub-chunk's columns
-          const int col = gtid & 63, which = gtid >> 6;
-          const int ccol = h * 64 + col;  // column within the chunk
-          float val = 0.f;
-          if (ccol < pl.rows_kv) {
-            int rem = ccol;
-            bool ok = true;
-            long long tok = 0;
-#pragma unroll
-            for (int a = 2; a >= 0; --a) {
-              if (a >= RANK) continue;
-              const int cc = org[a] + (a == 0 ? rem : rem % pl.ckv[a]);
-              if (a > 0) rem /= pl.ckv[a];
-              ok = ok && cc < t.Lr[a];
-              tok += (long long)(t.r[a] + g.dil[a] * cc) * g.tstride[a];
-            }
-            if (ok) {
-              tok += (long long)t.bh * g.N;
-              val = which == 0 ? lse[tok] * kLog2e : dvec[tok];
-            }
-          }
-          cv[which * 64 + col] = val;
-          ptx::named_bar_sync(1 + grp, 128);
+          if (u + 2 < nsub) next_val = fetch(u + 2);  // lands while this sub-chunk computes
         }
         const uint32_t buf = (gu & 1) * 64;
         if (tracer) NA_TRACE_EV(2 + grp, tr, 19);
@@ -368,6 +387,12 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar + B_P + (gu & 1));
         if (tracer) NA_TRACE_EV(2 + grp, tr, 21);
+        if constexpr (KV_STATIONARY) {
+          if (u + 2 < nsub) {  // publish the prefetched values for the next sub-chunk
+            vec[(grp * 2 + ((it + 1) & 1)) * 128 + (gtid >> 6) * 64 + (gtid & 63)] = next_val;
+            ptx::named_bar_sync(1 + grp, 128);
+          }
+        }
       }
       if (tracer) NA_TRACE_EV(2 + grp, tr, 22);
       // ---- epilogue (overlaps the next tile's MMAs) ----
@@ -410,7 +435,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
