@@ -135,13 +135,19 @@ def init_dist():
     return world, rank, local
 
 
-def reduce_max(x: float, world: int) -> float:
+def reduce_max(x: float, world: int, device: str = "cuda") -> float:
+    """Max over ranks (timings: the slowest rank defines the step)."""
     if world == 1:
         return x
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def shard_range(rank: int, bh_per_rank: int) -> tuple:
+    """Weak scaling: rank r owns global (b,h) slices [r*bh, (r+1)*bh)."""
+    return (rank * bh_per_rank, (rank + 1) * bh_per_rank)
 
 
 def barrier(world: int):
@@ -161,7 +167,7 @@ class Runner:
         self.cfgs = [na_synth.CONFIGS[v] for v in VARIANTS]
         c = self.cfgs[0]
         bh = c.batch * c.heads
-        rng = (rank * bh, (rank + 1) * bh)  # weak scaling: this rank's own B*H slices
+        rng = shard_range(rank, bh)  # weak scaling: this rank's own B*H slices
         q, k, v, do = na_synth.make_inputs(c, device="cuda", bh_range=rng)
         shape = c.shape()
         self.q, self.k, self.v, self.do = (t.view(shape) for t in (q, k, v, do))
