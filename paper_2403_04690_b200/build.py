@@ -40,6 +40,7 @@ def up_to_date() -> bool:
 def _compile(src: str, verbose: bool, bdir: str = BUILD, trace: bool = False) -> str:
     obj = os.path.join(bdir, os.path.basename(src) + ".o")
     extra = (["-Xptxas", "-v"] if verbose else []) + (["-DNA_TRACE"] if trace else [])
+    extra += [f"-D{d}" for d in os.environ.get("NA_DEFINES", "").split() if d]
     cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -82,12 +82,22 @@ enum : int {
   B_COUNT = B_OE + 2
 };
 
+// Tensor maps of one backward kernel: stationary tiles a0, a1; streamed
+// chunks b0, b1; output tiles out0 (, out1) stored with TMA (stationary box).
+struct BwdMaps {
+  CUtensorMap a0, a1, b0, b1, out0, out1;
+};
+
 template <int RANK, int D, bool BF16, bool KV_STATIONARY>
-__device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtensorMap& map_a1,
-                                         const CUtensorMap& map_b0, const CUtensorMap& map_b1,
-                                         const Geom& g, const TcPlan& pl, const float* __restrict__ lse,
-                                         const float* __restrict__ dvec, void* __restrict__ out0,
-                                         void* __restrict__ out1, unsigned num_tiles) {
+__device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, const TcPlan& pl,
+                                         const float* __restrict__ lse, const float* __restrict__ dvec,
+                                         unsigned num_tiles) {
+  const CUtensorMap& map_a0 = maps.a0;
+  const CUtensorMap& map_a1 = maps.a1;
+  const CUtensorMap& map_b0 = maps.b0;
+  const CUtensorMap& map_b1 = maps.b1;
+  const CUtensorMap& map_out0 = maps.out0;
+  const CUtensorMap& map_out1 = maps.out1;
   using S = BwdSmem<D>;
   using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -101,7 +111,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(bar + B_AF + b, 1);
-      ptx::mbar_init(bar + B_AE + b, 1);
+      ptx::mbar_init(bar + B_AE + b, KV_STATIONARY ? 2 : 1);  // released by the store issuers
       ptx::mbar_init(bar + B_S + b, 1);
       ptx::mbar_init(bar + B_P + b, 128);
       ptx::mbar_init(bar + B_OF + b, 1);
@@ -205,7 +215,6 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
                         ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
         }
         ptx::mma_commit_w(bar + B_S + (gu & 1));
-        if (u == nsub - 1) ptx::mma_commit_w(bar + B_AE + ab);  // stationary tiles reusable
       };
       ptx::mbar_wait(bar + B_AF + ab, (ti >> 1) & 1);
       ptx::tc_fence_after();
@@ -364,7 +373,8 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
               x1.y = (w >> (c + 3)) & 1u ? x1.y : -INFINITY;
             }
             const float2 p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
-            const float2 p1 = exp2_poly2(x1);                                // FMA pipe
+            const float2 p1 = use_poly(c) ? exp2_poly2(x1)                   // FMA pipe
+                                          : make_float2(ptx::ex2(x1.x), ptx::ex2(x1.y));
             const float2 ds0 = __fmul2_rn(p0, __fadd2_rn(make_float2(__uint_as_float(pv[c]),
                                                                      __uint_as_float(pv[c + 1])),
                                                          make_float2(-dd4.x, -dd4.y)));
@@ -396,15 +406,21 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
       }
       if (tracer) NA_TRACE_EV(2 + grp, tr, 22);
       // ---- epilogue (overlaps the next tile's MMAs) ----
+      // Every MMA of the tile is complete once the outputs are final, so the
+      // tile's stationary smem tiles are dead: stage the outputs there in the
+      // TMA box layout (same swizzle) and write them with TMA stores (rows
+      // past a ragged class end are clipped by the hardware).  The buffers
+      // return to the producer (B_AE) once the stores have read them.
+      // KV-stationary: group 0 stages dK (x scale) in the K tile, group 1 dV
+      // in the V tile.  Q-stationary: the groups split dQ's columns in the Q tile.
       ptx::mbar_wait(bar + B_OF + ob, (ti >> 1) & 1);
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 24);
       ptx::tc_fence_after();
-      // KV-stationary: group 0 writes dK (x scale), group 1 writes dV.
-      // Q-stationary: the two groups split dQ's D columns.
-      const long long off = r.out_offset(g, t);
+      const int ab = ti & 1;
+      uint8_t* stage = smem + S::kA + (2 * ab + (KV_STATIONARY ? grp : 0)) * S::kTile;
       constexpr int kCols = KV_STATIONARY ? D : D / 2;
+      const int col0 = KV_STATIONARY ? 0 : grp * (D / 2);   // first column this group writes
       const uint32_t src = kColOut + ob * 128 + (KV_STATIONARY ? grp * D : grp * (D / 2));
-      T* dst = reinterpret_cast<T*>(KV_STATIONARY && grp ? out1 : out0) + off +
-               (KV_STATIONARY ? 0 : grp * (D / 2));
       const float mul = (KV_STATIONARY && grp) ? 1.f : g.scale;
 #pragma unroll
       for (int c0 = 0; c0 < kCols; c0 += 16) {
@@ -416,22 +432,37 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
               "=r"(ov[13]), "=r"(ov[14]), "=r"(ov[15])
             : "r"(trow + src + c0));
         ptx::tmem_ld_wait();
-        if (r.valid) {
-          uint32_t pk[8];
+        uint32_t pk[8];
 #pragma unroll
-          for (int c = 0; c < 16; c += 2)
-            pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
-          uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
-          d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        }
+        for (int c = 0; c < 16; c += 2)
+          pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
+        const int chunk = (col0 + c0) / 8;
+        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk, S::kRowBytes)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + 1, S::kRowBytes)) =
+            make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(bar + B_OE + ob);
+      ptx::fence_proxy_async();  // staged tile visible to the TMA engine
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 25);
+      const bool issuer = KV_STATIONARY ? (gtid == 0) : (threadIdx.x == 0);
+      if constexpr (KV_STATIONARY) ptx::named_bar_sync(3 + grp, 128);
+      else ptx::named_bar_sync(3, kCompute);
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 26);
+      if (issuer) {
+        const CUtensorMap* om = (KV_STATIONARY && grp) ? &map_out1 : &map_out0;
+        for (int i = 0; i < pl.q_issues; ++i)
+          t.template store_box<RANK>(om, stage + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
+        ptx::bulk_commit();
+        ptx::bulk_wait_read<0>();
+        ptx::mbar_arrive(bar + B_AE + ab);  // stationary tiles reusable
+      }
       if (tracer) NA_TRACE_EV(2 + grp, tr, 23);
       ub += nsub;
       ++ti;
     }
+    if (KV_STATIONARY ? (gtid == 0) : (threadIdx.x == 0)) ptx::bulk_wait<0>();  // stores done before exit
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -444,28 +475,22 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap& map_a0, const CUtens
 // dK, dV: key-stationary over the inverse halo.
 template <int RANK, int D, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    fna_dkdv_tc(const __grid_constant__ CUtensorMap map_k, const __grid_constant__ CUtensorMap map_v,
-                const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_do,
-                Geom g, TcPlan pl, const float* __restrict__ lse, const float* __restrict__ dvec,
-                void* __restrict__ dk, void* __restrict__ dv, unsigned num_tiles) {
-  bwd_body<RANK, D, BF16, true>(map_k, map_v, map_q, map_do, g, pl, lse, dvec, dk, dv, num_tiles);
+    fna_dkdv_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, const float* __restrict__ lse,
+                const float* __restrict__ dvec, unsigned num_tiles) {
+  bwd_body<RANK, D, BF16, true>(maps, g, pl, lse, dvec, num_tiles);
 }
 
 // dQ: query-stationary over the forward halo.
 template <int RANK, int D, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    fna_dq_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_do,
-              const __grid_constant__ CUtensorMap map_k, const __grid_constant__ CUtensorMap map_v,
-              Geom g, TcPlan pl, const float* __restrict__ lse, const float* __restrict__ dvec,
-              void* __restrict__ dq, unsigned num_tiles) {
-  bwd_body<RANK, D, BF16, false>(map_q, map_do, map_k, map_v, g, pl, lse, dvec, dq, nullptr, num_tiles);
+    fna_dq_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, const float* __restrict__ lse,
+              const float* __restrict__ dvec, unsigned num_tiles) {
+  bwd_body<RANK, D, BF16, false>(maps, g, pl, lse, dvec, num_tiles);
 }
 
 template <int RANK, int D, bool BF16>
-cudaError_t launch_both(const Geom& g, const TcPlan& pl, const CUtensorMap* m, const float* lse,
-                        const float* dvec, void* dq, void* dk, void* dv, cudaStream_t st) {
-  // m: [0] Q tile, [1] K tile, [2] V tile, [3] dO tile, [4] Q chunk, [5] K chunk,
-  //    [6] V chunk, [7] dO chunk
+cudaError_t launch_both(const Geom& g, const TcPlan& pl, const BwdMaps& mkv, const BwdMaps& mq,
+                        const float* lse, const float* dvec, cudaStream_t st) {
   const int smem = BwdSmem<D>::kBytes + 1024;
   auto kdkdv = fna_dkdv_tc<RANK, D, BF16>;
   auto kdq = fna_dq_tc<RANK, D, BF16>;
@@ -481,26 +506,25 @@ cudaError_t launch_both(const Geom& g, const TcPlan& pl, const CUtensorMap* m, c
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const unsigned grid = (unsigned)(tiles < num_sms() ? tiles : num_sms());
   prof_begin(KID_DKDV_TC, st);
-  kdkdv<<<grid, kThreads, smem, st>>>(m[1], m[2], m[4], m[7], g, pl, lse, dvec, dk, dv, (unsigned)tiles);
+  kdkdv<<<grid, kThreads, smem, st>>>(mkv, g, pl, lse, dvec, (unsigned)tiles);
   prof_end(st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   prof_begin(KID_DQ_TC, st);
-  kdq<<<grid, kThreads, smem, st>>>(m[0], m[3], m[5], m[6], g, pl, lse, dvec, dq, (unsigned)tiles);
+  kdq<<<grid, kThreads, smem, st>>>(mq, g, pl, lse, dvec, (unsigned)tiles);
   prof_end(st);
   return cudaGetLastError();
 }
 
 template <int RANK>
-cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const CUtensorMap* m,
-                    const float* lse, const float* dvec, void* dq, void* dk, void* dv,
-                    cudaStream_t st) {
+cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const BwdMaps& mkv, const BwdMaps& mq,
+                    const float* lse, const float* dvec, cudaStream_t st) {
   const bool bf = dtype == 2;
   if (g.D == 64)
-    return bf ? launch_both<RANK, 64, true>(g, pl, m, lse, dvec, dq, dk, dv, st)
-              : launch_both<RANK, 64, false>(g, pl, m, lse, dvec, dq, dk, dv, st);
-  return bf ? launch_both<RANK, 32, true>(g, pl, m, lse, dvec, dq, dk, dv, st)
-            : launch_both<RANK, 32, false>(g, pl, m, lse, dvec, dq, dk, dv, st);
+    return bf ? launch_both<RANK, 64, true>(g, pl, mkv, mq, lse, dvec, st)
+              : launch_both<RANK, 64, false>(g, pl, mkv, mq, lse, dvec, st);
+  return bf ? launch_both<RANK, 32, true>(g, pl, mkv, mq, lse, dvec, st)
+            : launch_both<RANK, 32, false>(g, pl, mkv, mq, lse, dvec, st);
 }
 
 }  // namespace
@@ -513,21 +537,29 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   cudaError_t e = bwd_preprocess(dtype, g, o, d_o, Dvec, st);
   if (e != cudaSuccess) return e;
   TcPlan pl = make_plan(g, 128);
-  CUtensorMap m[8];
-  const void* ptrs[4] = {q, k, v, d_o};
-  for (int i = 0; i < 4; ++i) {
-    if ((e = make_map(&m[i], dtype, g, ptrs[i], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
-    if ((e = make_map(&m[4 + i], dtype, g, ptrs[i], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+  // dK/dV kernel: stationary K, V tiles; streamed Q, dO chunks; outputs dK, dV.
+  // dQ kernel: stationary Q, dO tiles; streamed K, V chunks; output dQ.
+  BwdMaps mkv, mq;
+  const void* tile_src[2][2] = {{k, v}, {q, d_o}};
+  const void* chunk_src[2][2] = {{q, d_o}, {k, v}};
+  BwdMaps* mm[2] = {&mkv, &mq};
+  for (int w = 0; w < 2; ++w) {
+    if ((e = make_map(&mm[w]->a0, dtype, g, tile_src[w][0], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+    if ((e = make_map(&mm[w]->a1, dtype, g, tile_src[w][1], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+    if ((e = make_map(&mm[w]->b0, dtype, g, chunk_src[w][0], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+    if ((e = make_map(&mm[w]->b1, dtype, g, chunk_src[w][1], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
   }
+  if ((e = make_map(&mkv.out0, dtype, g, dk, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mkv.out1, dtype, g, dv, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mq.out0, dtype, g, dq, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+  mq.out1 = mq.out0;
   *launches = 3;
   switch (g.rank) {
-    case 1: return by_type<1>(dtype, g, pl, m, lse, Dvec, dq, dk, dv, st);
-    case 2: return by_type<2>(dtype, g, pl, m, lse, Dvec, dq, dk, dv, st);
-    default: return by_type<3>(dtype, g, pl, m, lse, Dvec, dq, dk, dv, st);
+    case 1: return by_type<1>(dtype, g, pl, mkv, mq, lse, Dvec, st);
+    case 2: return by_type<2>(dtype, g, pl, mkv, mq, lse, Dvec, st);
+    default: return by_type<3>(dtype, g, pl, mkv, mq, lse, Dvec, st);
   }
 }
-
-}  // namespace na
 
 #ifdef NA_TRACE
 // Trace build only (libna_trace.so): point the backward kernels' event buffer.
@@ -536,3 +568,5 @@ extern "C" int na_debug_set_trace_bwd(void* p, int which) {
   return cudaMemcpyToSymbol(na::g_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 1;
 }
 #endif
+
+}  // namespace na

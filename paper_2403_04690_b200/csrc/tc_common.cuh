@@ -51,6 +51,19 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(p.x) + ex), __int_as_float(__float_as_int(p.y) + ey));
 }
 
+// Which exponentials go to the FMA-pipe polynomial: the element pair at
+// column c (c % 4 == 2 within each group of 4).  The softmax loops are
+// issue-bound as well as MUFU-bound, and the polynomial costs ~6 issue slots
+// per element against ~1 for MUFU, so only part of the elements take it.
+// NA_POLY_MODE: 0 none, 1 one pair in four groups-of-two (25%), 2 every
+// second pair (50%).
+#ifndef NA_POLY_MODE
+#define NA_POLY_MODE 1
+#endif
+__device__ __forceinline__ constexpr bool use_poly(int c) {
+  return NA_POLY_MODE == 2 ? true : (NA_POLY_MODE == 1 ? (c & 4) != 0 : false);
+}
+
 // Which (b*h, residue class, tile) a CTA owns, and the tile's halo.
 // `tile` = the 128-token box this CTA is stationary on (queries in the
 // forward and dQ kernels, keys in the dK/dV kernel); `inverse` selects
@@ -135,6 +148,21 @@ struct TileCtx {
     } else {
       ptx::tma_load_5d_w(dst, m, bar, 0, r[2] + g.dil[2] * (org[2] + x_off),
                        r[1] + g.dil[1] * org[1], r[0] + g.dil[0] * org[0], bh);
+    }
+  }
+
+  // TMA store of the stationary tile's box (one thread issues).
+  template <int R>
+  __device__ __forceinline__ void store_box(const CUtensorMap* m, const void* src, int x_off,
+                                            const Geom& g) const {
+    if constexpr (R == 1) {
+      ptx::tma_store_3d(m, src, 0, r[0] + g.dil[0] * (q_origin[0] + x_off), bh);
+    } else if constexpr (R == 2) {
+      ptx::tma_store_4d(m, src, 0, r[1] + g.dil[1] * (q_origin[1] + x_off), r[0] + g.dil[0] * q_origin[0],
+                        bh);
+    } else {
+      ptx::tma_store_5d(m, src, 0, r[2] + g.dil[2] * (q_origin[2] + x_off), r[1] + g.dil[1] * q_origin[1],
+                        r[0] + g.dil[0] * q_origin[0], bh);
     }
   }
 };

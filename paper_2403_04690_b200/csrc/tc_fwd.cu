@@ -72,11 +72,19 @@ enum : int {
   B_COUNT = B_OE + 2
 };
 
+// Tensor maps: Q tiles, K and V chunks, and O tiles (TMA store, Q's box).
+struct FwdMaps {
+  CUtensorMap q, k, v, o;
+};
+
 template <int RANK, int D, bool BF16>
 __global__ void __launch_bounds__(kThreads, 2)
-    fna_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-               const __grid_constant__ CUtensorMap map_v, Geom g, TcPlan pl, void* __restrict__ o_ptr,
-               float* __restrict__ lse, unsigned num_tiles) {
+    fna_fwd_tc(const __grid_constant__ FwdMaps maps, Geom g, TcPlan pl, float* __restrict__ lse,
+               unsigned num_tiles) {
+  const CUtensorMap& map_q = maps.q;
+  const CUtensorMap& map_k = maps.k;
+  const CUtensorMap& map_v = maps.v;
+  const CUtensorMap& map_o = maps.o;
   using S = FwdSmem<D>;
   using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -184,7 +192,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                         ptx::make_sdesc(k_addr + kk * 32, 16, kSbo, kSw), h ? idesc_s1 : idesc_s0,
                         kk > 0);
         ptx::mma_commit_w(bar + B_S + (gu & 1));
-        if (u == nsub - 1) ptx::mma_commit_w(bar + B_QE + qb);  // Q buffer reusable
       };
       ptx::mbar_wait(bar + B_QF + qb, (ti >> 1) & 1);
       ptx::tc_fence_after();
@@ -312,7 +319,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(s4[2]), __uint_as_float(s4[3])),
                                          make_float2(sl2, sl2), make_float2(nmu, nmu));
             const float2 p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
-            const float2 p1 = exp2_poly2(x1);                                // FMA pipe
+            const float2 p1 = use_poly(c) ? exp2_poly2(x1)                   // FMA pipe
+                                          : make_float2(ptx::ex2(x1.x), ptx::ex2(x1.y));
             acc0 = __fadd2_rn(acc0, p0);
             acc1 = __fadd2_rn(acc1, p1);
             pk[16 * gq + (c >> 1)] = pack2<BF16>(p0.x, p0.y);
@@ -326,32 +334,48 @@ __global__ void __launch_bounds__(kThreads, 2)
         ptx::mbar_arrive(bar + B_P + (gu & 1));
       }
       // ---- epilogue: O / l, LSE (overlaps the next tile's S MMAs) ----
+      // All MMAs of the tile are complete once O is final, so the tile's Q
+      // buffer is dead: stage the normalised O there (TMA box layout, same
+      // swizzle) and write it with one TMA store, which also clips rows past
+      // a ragged class end.  The buffer returns to the producer (B_QE) once
+      // the store has read it.
       ptx::mbar_wait(bar + B_OF + ob, (ti >> 1) & 1);
       ptx::tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      const long long ooff = r.out_offset(g, t);
-      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(o_ptr) + ooff);
+      const int qb = ti & 1;
+      uint8_t* stage = smem + S::kQ + qb * S::kTile;
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t ov[32];
         NA_TMEM_LD32(trow + o_col + c0, ov);
         ptx::tmem_ld_wait();
-        if (r.valid) {
 #pragma unroll
-          for (int c = 0; c < 32; c += 8)
-            dst[(c0 + c) / 8] =
-                make_uint4(pack2<BF16>(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv),
-                           pack2<BF16>(__uint_as_float(ov[c + 2]) * inv, __uint_as_float(ov[c + 3]) * inv),
-                           pack2<BF16>(__uint_as_float(ov[c + 4]) * inv, __uint_as_float(ov[c + 5]) * inv),
-                           pack2<BF16>(__uint_as_float(ov[c + 6]) * inv, __uint_as_float(ov[c + 7]) * inv));
-        }
+        for (int c = 0; c < 32; c += 8)
+          *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, (c0 + c) / 8, S::kRowBytes)) =
+              make_uint4(pack2<BF16>(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv),
+                         pack2<BF16>(__uint_as_float(ov[c + 2]) * inv, __uint_as_float(ov[c + 3]) * inv),
+                         pack2<BF16>(__uint_as_float(ov[c + 4]) * inv, __uint_as_float(ov[c + 5]) * inv),
+                         pack2<BF16>(__uint_as_float(ov[c + 6]) * inv, __uint_as_float(ov[c + 7]) * inv));
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(bar + B_OE + ob);  // O buffer may be overwritten by tile ti + 2
-      if (lse && r.valid) lse[ooff / g.D] = (m_ref + __log2f(l)) * 0.69314718055994531f;
+      ptx::fence_proxy_async();           // staged O visible to the TMA engine
+      ptx::named_bar_sync(1, kSoftmax);
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < pl.q_issues; ++i)
+          t.template store_box<RANK>(&map_o, stage + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
+        ptx::bulk_commit();
+        ptx::bulk_wait_read<0>();
+        ptx::mbar_arrive(bar + B_QE + qb);  // Q buffer reusable
+      }
+      if (lse && r.valid) {
+        const long long ooff = r.out_offset(g, t);
+        lse[ooff / g.D] = (m_ref + __log2f(l)) * 0.69314718055994531f;
+      }
       ub += nsub;
       ++ti;
     }
+    if (threadIdx.x == 0) ptx::bulk_wait<0>();  // all O stores complete before exit
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -362,8 +386,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 template <int RANK, int D, bool BF16>
-cudaError_t launch(const Geom& g, const TcPlan& pl, const CUtensorMap& mq, const CUtensorMap& mk,
-                   const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
+cudaError_t launch(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse, cudaStream_t st) {
   auto kern = fna_fwd_tc<RANK, D, BF16>;
   const int smem = FwdSmem<D>::kBytes + 1024;
   static bool attr = false;  // benign race: idempotent
@@ -376,20 +399,18 @@ cudaError_t launch(const Geom& g, const TcPlan& pl, const CUtensorMap& mq, const
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const unsigned grid = (unsigned)(tiles < 2LL * num_sms() ? tiles : 2LL * num_sms());
   prof_begin(KID_FWD_TC, st);
-  kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, g, pl, o, lse, (unsigned)tiles);
+  kern<<<grid, kThreads, smem, st>>>(maps, g, pl, lse, (unsigned)tiles);
   prof_end(st);
   return cudaGetLastError();
 }
 
 template <int RANK>
-cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const CUtensorMap& mq,
-                    const CUtensorMap& mk, const CUtensorMap& mv, void* o, float* lse,
+cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse,
                     cudaStream_t st) {
   const bool bf = dtype == 2;
-  if (g.D == 64) return bf ? launch<RANK, 64, true>(g, pl, mq, mk, mv, o, lse, st)
-                           : launch<RANK, 64, false>(g, pl, mq, mk, mv, o, lse, st);
-  return bf ? launch<RANK, 32, true>(g, pl, mq, mk, mv, o, lse, st)
-            : launch<RANK, 32, false>(g, pl, mq, mk, mv, o, lse, st);
+  if (g.D == 64) return bf ? launch<RANK, 64, true>(g, pl, maps, lse, st)
+                           : launch<RANK, 64, false>(g, pl, maps, lse, st);
+  return bf ? launch<RANK, 32, true>(g, pl, maps, lse, st) : launch<RANK, 32, false>(g, pl, maps, lse, st);
 }
 
 }  // namespace
@@ -399,16 +420,17 @@ cudaError_t tc_fwd(int dtype, const Geom& g, const void* q, const void* k, const
   const char* why;
   if (!tc_supported(dtype, g, &why)) return cudaErrorNotSupported;
   TcPlan pl = make_plan(g, /*q_tile_rows=*/128);
-  CUtensorMap mq, mk, mv;
+  FwdMaps maps;
   cudaError_t e;
-  if ((e = make_map(&mq, dtype, g, q, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&mk, dtype, g, k, pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&mv, dtype, g, v, pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&maps.q, dtype, g, q, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&maps.k, dtype, g, k, pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&maps.v, dtype, g, v, pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&maps.o, dtype, g, o, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
   *launches = 1;
   switch (g.rank) {
-    case 1: return by_type<1>(dtype, g, pl, mq, mk, mv, o, lse, st);
-    case 2: return by_type<2>(dtype, g, pl, mq, mk, mv, o, lse, st);
-    default: return by_type<3>(dtype, g, pl, mq, mk, mv, o, lse, st);
+    case 1: return by_type<1>(dtype, g, pl, maps, lse, st);
+    case 2: return by_type<2>(dtype, g, pl, maps, lse, st);
+    default: return by_type<3>(dtype, g, pl, maps, lse, st);
   }
 }
 

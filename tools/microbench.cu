@@ -99,6 +99,32 @@ __global__ void k_mufu(unsigned long long* out, int iters, int nwarps, float* si
   if (s == 12345.f) sink[0] = s;
 }
 
+__global__ void k_mufu16(unsigned long long* out, int iters, int nwarps, float* sink) {
+  const int warp = threadIdx.x >> 5;
+  uint32_t x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = 0xBC00BC00u ^ (threadIdx.x + c);  // ~ -1.0 halves
+  __syncthreads();
+  const unsigned long long t0 = clock64();
+  if (warp < nwarps) {
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t y;
+        asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x[c]));
+        x[c] = y ^ 0x80008000u;  // keep values negative, dependent chain
+      }
+    }
+  }
+  __syncthreads();
+  const unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  uint32_t s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s ^= x[c];
+  if (s == 12345u) sink[0] = (float)s;
+}
+
 __global__ void k_ffma2(unsigned long long* out, int iters, int nwarps, float* sink) {
   const int warp = threadIdx.x >> 5;
   float2 x[8];
@@ -191,6 +217,10 @@ int main() {
     cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
     const double cyc = avg(h, sms);
     printf("mufu  warps=%2d: %.2f ex2/clk/SM\n", nw, nw * 32.0 * 8 * iters / cyc);
+    k_mufu16<<<sms, 32 * 16>>>(d, iters, nw, sink);
+    cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
+    const double ch = avg(h, sms);
+    printf("mufu16x2 warps=%2d: %.2f ex2 results/clk/SM (f16x2: 2 per op)\n", nw, nw * 32.0 * 16 * iters / ch);
     k_ffma2<<<sms, 32 * 16>>>(d, iters, nw, sink);
     cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
     const double cf = avg(h, sms);

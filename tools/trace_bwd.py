@@ -43,32 +43,17 @@ ev1.record()
 torch.cuda.synchronize()
 print(f"{name}: backward {ev0.elapsed_time(ev1):.3f} ms (kernel {which})")
 t = buf.view(64, 4, 256).cpu()
-for cta in (0, 1, 37):
-    evs = []
+import collections
+for cta in (0, 37):
+    print(f"--- CTA {cta}")
     for role in range(4):
-        for x in t[cta, role].tolist():
-            if x == 0:
-                break
-            evs.append(((x >> 8), role, x & 0xFF))
-    if not evs:
-        continue
-    t0 = min(e[0] for e in evs)
-    evs.sort()
-    print(f"--- CTA {cta}: {len(evs)} events, span {evs[-1][0] - t0} cycles")
-    line = []
-    for c, role, tag in evs[:140]:
-        line.append(f"{c - t0:>7}:{tag}")
-        if len(line) == 10:
-            print("  " + "  ".join(line))
-            line = []
-    if line:
-        print("  " + "  ".join(line))
-    # per-event-type mean gaps
-    import collections
-    by = collections.defaultdict(list)
-    for c, role, tag in evs:
-        by[tag].append(c)
-    for tag, cs in sorted(by.items()):
-        if len(cs) > 2:
-            d = [b - a for a, b in zip(cs, cs[1:])]
-            print(f"   tag {tag:2d}: n={len(cs):3d} mean gap {sum(d) / len(d):8.1f} cycles")
+        evs = [((x >> 8), x & 0xFF) for x in t[cta, role].tolist() if x != 0]
+        if not evs:
+            continue
+        t0 = evs[0][0]
+        print(f"  role {role}: " + "  ".join(f"{c - t0}:{tag}" for c, tag in evs[:40]))
+        by = collections.defaultdict(list)
+        for i2 in range(1, len(evs)):
+            by[(evs[i2 - 1][1], evs[i2][1])].append(evs[i2][0] - evs[i2 - 1][0])
+        print("     mean gaps: " + ", ".join(f"{a}->{b}: {sum(v) / len(v):.0f} (n={len(v)})"
+                                            for (a, b), v in sorted(by.items()) if len(v) > 3))
