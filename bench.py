@@ -176,7 +176,10 @@ class Runner:
             o = torch.empty(shape, dtype=c.dtype, device="cuda")
             lse = torch.empty(shape[:-1], dtype=torch.float32, device="cuda")
             grads = [torch.empty(shape, dtype=c.dtype, device="cuda") for _ in range(3)]
-            ws = torch.empty(c.batch * c.heads * c.tokens, dtype=torch.float32, device="cuda")
+            pr = na.make_problem(batch=c.batch, heads=c.heads, extent=list(c.extent), head_dim=c.head_dim,
+                                 kernel_size=list(cfg.kernel_size), dilation=list(cfg.dilation),
+                                 is_causal=[bool(x) for x in cfg.is_causal], dtype=c.dtype)
+            ws = torch.empty((na.na_bwd_workspace_size(pr) + 3) // 4, dtype=torch.float32, device="cuda")
             self.outs.append((o, lse, grads, ws))
         self.launches = 0
 

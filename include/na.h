@@ -102,8 +102,11 @@ na_status na_validate(const na_problem* p);
 na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* v, void* o,
                  float* lse, void* stream);
 
-/* Bytes of device workspace na_bwd needs: batch*heads*prod(extent)*4
- * (the fp32 row vector D_x = <dO_x, O_x>). */
+/* Bytes of device workspace na_bwd needs for the fp32 row vectors
+ * D_x = <dO_x, O_x> and, on the tensor-core path, -LSE_x*log2(e):
+ * max(B*H*N*4, B*H*nres*2*plane*4) with nres = prod(dilation) residue
+ * classes and plane = prod_a ceil(extent_a / dilation_a), the innermost factor
+ * rounded up to a multiple of 4 (class-compacted layout, 16-byte TMA strides). */
 size_t na_bwd_workspace_size(const na_problem* p);
 
 /* Backward.  Reads q, k, v, o, d_o (dL/dO) and lse from na_fwd on the same

@@ -142,25 +142,75 @@ __global__ void __launch_bounds__(256) fna_bwd_pre(Geom g, const T* __restrict__
 // D_x for 16-bit rows: each thread reads 16 bytes (8 elements) of O and dO,
 // D/8 consecutive threads own a row and reduce with shuffles (fully
 // coalesced 16-byte loads; the kernel is HBM-bound).
+// Row-vector mode (lse != nullptr, tensor-core path): instead of D_x at the
+// token's index, writes the pair (-LSE_x * log2(e), D_x) into the two planes
+// of the class-compacted layout (na_geom.cuh, Geom::rv_*), so the backward
+// kernels fetch a chunk's partner values with one TMA box.
+__device__ __forceinline__ long long rv_index(const Geom& g, long long row) {
+  // 32-bit division (a 64-bit one is emulated and dominated this HBM-bound
+  // kernel); B*H*N < 2^32 for any problem whose tensors fit in memory.
+  const unsigned r32 = (unsigned)row;
+  const int bh = (int)(r32 / (unsigned)g.N);
+  const int n = (int)(r32 - (unsigned)bh * (unsigned)g.N);
+  int res = 0;
+  long long off = 0;
+  if (g.rank == 1) {  // fast path: one division (none without dilation)
+    const int d = g.dil[0];
+    const int c = d == 1 ? n : n / d;
+    res = n - c * d;
+    off = c;
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {  // constant indices: Geom stays in the param space
+      if (a < g.rank) {
+        const int x = (n / g.tstride[a]) % g.L[a];
+        res = res * g.dil[a] + x % g.dil[a];
+        off += (long long)(x / g.dil[a]) * g.rv_cs[a];
+      }
+    }
+  }
+  return rv_base(g, bh, res) + off;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restrict__ o,
                                                        const T* __restrict__ d_o,
-                                                       float* __restrict__ Dvec) {
-  const int tpr = g.D / 8;  // threads per row (power of two: D in {8,...,256} multiple of 8)
+                                                       float* __restrict__ Dvec,
+                                                       const float* __restrict__ lse) {
+  // D/8 threads per row; only the tensor-core path (D in {32, 64}) launches
+  // this kernel, so tpr is a power of two: shift/mask, no 64-bit division.
+  const int tpr = g.D / 8;
+  const int shift = __ffs(tpr) - 1;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t row = gid / tpr;
-  const int part = (int)(gid % tpr);
+  const int64_t row = gid >> shift;
+  const int part = (int)(gid & (tpr - 1));
+  const bool valid = row < (int64_t)g.BH * g.N;
+  // Row-vector mode: LSE and the destination index first, so their latency
+  // overlaps the O/dO loads (one HBM round trip per warp, not two).
+  float l = 0.f;
+  long long i = 0;
+  if (lse && part == 0 && valid) {
+    l = lse[row];
+    i = rv_index(g, row);
+  }
   float s = 0.f;
-  if (row < (int64_t)g.BH * g.N) {
+  if (valid) {
     const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + row * g.D) + part);
     const uint4 b = __ldg(reinterpret_cast<const uint4*>(d_o + row * g.D) + part);
     const T* ea = reinterpret_cast<const T*>(&a);
     const T* eb = reinterpret_cast<const T*>(&b);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s = fmaf(ld_val(ea[i]), ld_val(eb[i]), s);
+    for (int e = 0; e < 8; ++e) s = fmaf(ld_val(ea[e]), ld_val(eb[e]), s);
   }
   for (int off = 1; off < tpr; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (part == 0 && row < (int64_t)g.BH * g.N) Dvec[row] = s;
+  if (part == 0 && valid) {
+    if (lse) {
+      Dvec[i] = -l * 1.4426950408889634f;
+      Dvec[i + g.rv_plane] = s;
+    } else {
+      Dvec[row] = s;
+    }
+  }
 }
 
 // ------------------------------------------------------------- bwd: dQ
@@ -353,20 +403,28 @@ cudaError_t simt_fwd(int dtype, const Geom& g, const void* q, const void* k, con
   }
 }
 
-cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, float* Dvec,
-                           cudaStream_t st) {
+cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, const float* lse,
+                           float* Dvec, cudaStream_t st) {
   const int64_t rows = (int64_t)g.BH * g.N;
   const unsigned grid = (unsigned)((rows + 7) / 8);
+  if (lse) {  // row-vector layout: slots no token maps to (ragged classes) must read as 0
+    bool ragged = g.rv_lc[g.rank - 1] * g.dil[g.rank - 1] != g.L[g.rank - 1];
+    for (int a = 0; a + 1 < g.rank; ++a) ragged = ragged || g.L[a] % g.dil[a] != 0;
+    if (ragged) {
+      cudaError_t e = cudaMemsetAsync(Dvec, 0, (size_t)g.BH * g.nres * 2 * g.rv_plane * sizeof(float), st);
+      if (e != cudaSuccess) return e;
+    }
+  }
   prof_begin(KID_BWD_PRE, st);
   const unsigned vgrid = (unsigned)((rows * (g.D / 8) + 255) / 256);
   switch (dtype) {
     case 0: fna_bwd_pre<float><<<grid, 256, 0, st>>>(g, (const float*)o, (const float*)d_o, Dvec); break;
     case 1:
-      fna_bwd_pre_vec<__half><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec);
+      fna_bwd_pre_vec<__half><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec, lse);
       break;
     default:
       fna_bwd_pre_vec<__nv_bfloat16><<<vgrid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
-                                                            (const __nv_bfloat16*)d_o, Dvec);
+                                                            (const __nv_bfloat16*)d_o, Dvec, lse);
   }
   prof_end(st);
   return cudaGetLastError();

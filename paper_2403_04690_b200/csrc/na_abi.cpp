@@ -70,6 +70,10 @@ na_status validate(const na_problem* p) {
     return fail(NA_ERR_SHAPE, "problem too large");
   if ((int64_t)p->batch * p->heads > 0x7fffffff || n > 0x7fffffff)
     return fail(NA_ERR_SHAPE, "B*H or tokens exceed int32");
+  // Row indices are 32-bit in the kernels; Q, K, V, O of 2^32 rows cannot fit
+  // in device memory at any head_dim.
+  if ((int64_t)p->batch * p->heads * n > (int64_t)0xffffffff)
+    return fail(NA_ERR_SHAPE, "B*H*tokens exceeds 2^32");
   if (p->impl != NA_IMPL_AUTO && p->impl != NA_IMPL_SIMT && p->impl != NA_IMPL_TC)
     return fail(NA_ERR_IMPL, "impl %d unknown", (int)p->impl);
   return NA_OK;
@@ -98,7 +102,27 @@ na::Geom make_geom(const na_problem* p) {
   for (int a = p->rank; a < 3; ++a) g.tstride[a] = 1;
   g.scale = p->scale > 0.f ? p->scale : 1.f / std::sqrt((float)p->head_dim);
   g.scale_log2 = g.scale * 1.4426950408889634f;
+  g.nres = 1;
+  for (int a = 0; a < 3; ++a) {
+    g.nres *= g.dil[a];
+    g.rv_lc[a] = (g.L[a] + g.dil[a] - 1) / g.dil[a];
+  }
+  g.rv_lc[p->rank - 1] = (g.rv_lc[p->rank - 1] + 3) / 4 * 4;
+  long long cs = 1;
+  for (int a = 2; a >= 0; --a) {
+    g.rv_cs[a] = (int)cs;
+    cs *= g.rv_lc[a];
+  }
+  g.rv_plane = cs;
   return g;
+}
+
+// Backward workspace: the SIMT path's D_x vector [BH*N] or the tensor-core
+// path's row-vector layout [BH*nres][2][plane], whichever is larger.
+size_t bwd_workspace_bytes(const na::Geom& g) {
+  const size_t simt = (size_t)g.BH * (size_t)g.N * sizeof(float);
+  const size_t tc = (size_t)g.BH * (size_t)g.nres * 2 * (size_t)g.rv_plane * sizeof(float);
+  return simt > tc ? simt : tc;
 }
 
 // Which family runs problem p (assumes p validated).
@@ -208,8 +232,7 @@ na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* 
 
 size_t na_bwd_workspace_size(const na_problem* p) {
   if (validate(p) != NA_OK) return 0;
-  na::Geom g = make_geom(p);
-  return (size_t)g.BH * (size_t)g.N * sizeof(float);
+  return bwd_workspace_bytes(make_geom(p));
 }
 
 na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* v, const void* o,
@@ -223,7 +246,7 @@ na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* 
   for (const void* ptr : ptrs)
     if (!aligned16(ptr)) return fail(NA_ERR_ALIGNMENT, "tensor base pointers must be 16-byte aligned");
   na::Geom g = make_geom(p);
-  const size_t need = (size_t)g.BH * (size_t)g.N * sizeof(float);
+  const size_t need = bwd_workspace_bytes(g);
   if (!workspace || workspace_bytes < need || !aligned16(workspace))
     return fail(NA_ERR_WORKSPACE, "workspace needs %zu bytes (16-byte aligned), got %zu", need,
                 workspace_bytes);

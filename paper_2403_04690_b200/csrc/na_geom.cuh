@@ -64,6 +64,19 @@ struct Geom {
   int tstride[3];  // token stride of each axis in the flat spatial index
   float scale;     // softmax scale
   float scale_log2;  // scale * log2(e)
+  // Backward row-vector layout (tensor-core path): per (b,h) and residue
+  // class, two planes [-LSE_x * log2(e) | D_x] indexed by compacted
+  // coordinates, rv_lc[a] = ceil(L/dil) per axis (innermost padded to a
+  // multiple of 4 so every TMA stride is a multiple of 16 bytes).
+  int nres;          // residue classes per (b,h) = prod dil
+  int rv_lc[3];      // compacted extent per axis (innermost padded)
+  int rv_cs[3];      // element stride per compacted axis
+  long long rv_plane;  // elements per plane = rv_cs[0] * rv_lc[0]
 };
+
+// Offset of plane 0 of class `res` of head `bh` in the row-vector layout.
+NA_HD long long rv_base(const Geom& g, int bh, int res) {
+  return ((long long)bh * g.nres + res) * 2 * g.rv_plane;
+}
 
 }  // namespace na

@@ -28,9 +28,11 @@ cudaError_t simt_bwd(int dtype, const Geom& g, const void* q, const void* k, con
                      const void* o, const void* d_o, const float* lse, void* dq, void* dk,
                      void* dv, float* Dvec, cudaStream_t st);
 
-// D_x = <dO_x, O_x> (fp32), one warp per row.
-cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, float* Dvec,
-                           cudaStream_t st);
+// D_x = <dO_x, O_x> (fp32).  lse == nullptr: D_x at the token index of Dvec
+// [BH*N].  lse != nullptr (16-bit only): the tensor-core row-vector layout
+// (-LSE_x*log2(e), D_x) of Geom::rv_* in Dvec.
+cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, const float* lse,
+                           float* Dvec, cudaStream_t st);
 
 // tcgen05 path.  tc_supported() is a pure host check; the launchers return
 // cudaErrorNotSupported for problems outside it.

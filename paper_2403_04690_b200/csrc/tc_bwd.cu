@@ -60,8 +60,8 @@ struct BwdSmem {
   static constexpr int kA = 0;                        // stationary [2 bufs][2 tiles] (K,V | Q,dO)
   static constexpr int kB0 = kA + 4 * kTile;          // streamed [kStages] (Q | K)
   static constexpr int kB1 = kB0 + kStages * kTile;   // streamed [kStages] (dO | V)
-  static constexpr int kVec = kB1 + kStages * kTile;  // [parity][slot][LSE2 x64 | D x64] fp32
-  static constexpr int kBar = kVec + 2 * 2 * 128 * 4;
+  static constexpr int kVec = kB1 + kStages * kTile;  // [kStages][-LSE2 x128 | D x128] fp32 (dK/dV)
+  static constexpr int kBar = kVec + kStages * 256 * 4;
   static constexpr int kBytes = kBar + 256;
 };
 
@@ -86,12 +86,12 @@ enum : int {
 // chunks b0, b1; output tiles out0 (, out1) stored with TMA (stationary box).
 struct BwdMaps {
   CUtensorMap a0, a1, b0, b1, out0, out1;
+  CUtensorMap rv;  // dK/dV: the streamed chunk's row vector (-LSE*log2(e), D)
 };
 
 template <int RANK, int D, bool BF16, bool KV_STATIONARY>
 __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, const TcPlan& pl,
-                                         const float* __restrict__ lse, const float* __restrict__ dvec,
-                                         unsigned num_tiles) {
+                                         const float* __restrict__ rv, unsigned num_tiles) {
   const CUtensorMap& map_a0 = maps.a0;
   const CUtensorMap& map_a1 = maps.a1;
   const CUtensorMap& map_b0 = maps.b0;
@@ -101,7 +101,9 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   using S = BwdSmem<D>;
   using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (LDS/STS, not generic LD/ST).
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + B_COUNT);
   float* vec = reinterpret_cast<float*>(smem + S::kVec);
@@ -123,6 +125,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     }
     ptx::fence_barrier_init();
   }
+  for (int i = threadIdx.x; i < kStages * 256; i += kThreads) vec[i] = 0.f;  // unloaded columns read 0
+  ptx::fence_proxy_async();  // before TMA writes the same smem
   if (pl.rows_kv < 128) {  // rows no TMA box writes must be finite (zero)
     const int nz = (128 - pl.rows_kv) * S::kRowBytes / 16;
     for (int i = threadIdx.x; i < 2 * kStages * nz; i += kThreads) {
@@ -144,13 +148,16 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     ptx::tma_prefetch(&map_a1);
     ptx::tma_prefetch(&map_b0);
     ptx::tma_prefetch(&map_b1);
-    const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes;
+    const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes + (KV_STATIONARY ? 2 * pl.rows_kv * 4 : 0);
     uint32_t kv_it = 0, ti = 0;
+    int tr = 0;
+    (void)tr;
     for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       TileCtx<RANK> t;
       if (!t.init(g, pl, tile, /*inverse=*/KV_STATIONARY)) continue;
       const int ab = ti & 1;
       if (ti >= 2) ptx::mbar_wait(bar + B_AE + ab, ((ti >> 1) - 1) & 1);
+      if (NA_BWD_TRACE_ON) NA_TRACE_EV(0, tr, 1);
       uint8_t* a0 = smem + S::kA + (2 * ab) * S::kTile;
       uint8_t* a1 = a0 + S::kTile;
       ptx::mbar_expect_tx_w(bar + B_AF + ab, 2 * 128 * S::kRowBytes);
@@ -163,6 +170,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       for (int j = 0; j < t.nchunks; ++j, ++kv_it) {
         const int s = kv_it % kStages;
         if (kv_it >= kStages) ptx::mbar_wait(bar + B_E + s, ((kv_it / kStages) - 1) & 1);
+        if (NA_BWD_TRACE_ON) NA_TRACE_EV(0, tr, 2);
         int org[3];
         t.chunk_origin(pl, j, org);
         ptx::mbar_expect_tx_w(bar + B_B + s, bytes);
@@ -172,6 +180,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           t.template load_box<RANK>(&map_b1, smem + S::kB1 + s * S::kTile + i * pl.kv_box_x * S::kRowBytes,
                                     bar + B_B + s, org, i * pl.kv_box_x, g);
         }
+        if constexpr (KV_STATIONARY) t.template load_rv<RANK>(&maps.rv, vec + s * 256, bar + B_B + s, org, g);
       }
       ++ti;
     }
@@ -183,44 +192,64 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     const uint32_t idesc_s0 = ptx::make_idesc(128, ns == 2 ? 64 : pl.n_kv, BF16, false);
     const uint32_t idesc_s1 = ptx::make_idesc(128, ns == 2 ? n1 : 16, BF16, false);
     constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
-    uint32_t kv_base = 0, ub = 0, ti = 0;
     int tr = 0;
     (void)tr;
-    for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      TileCtx<RANK> t;
-      if (!t.init(g, pl, tile, /*inverse=*/KV_STATIONARY)) continue;
-      const int nsub = t.nchunks * ns;
-      const int ab = ti & 1, ob = ti & 1;
+    // Issue cursor: the S/dP MMAs of sub-chunk (tile, u) run two sub-chunks
+    // ahead of the OUT MMAs, ACROSS tile boundaries, so the next tile's first
+    // sub-chunks are computed while this tile's last ones are consumed.
+    TileCtx<RANK> ct;
+    unsigned ctile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, ct);
+    uint32_t c_ti = 0, c_kv = 0, c_ub = 0;
+    int c_u = 0;
+    auto issue_next = [&]() {
+      if (ctile >= num_tiles) return;
+      const int ab = c_ti & 1;
+      if (c_u == 0) {
+        ptx::mbar_wait(bar + B_AF + ab, (c_ti >> 1) & 1);
+        if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 14);
+        ptx::tc_fence_after();
+      }
       const uint32_t a0 = ptx::smem_u32(smem + S::kA + (2 * ab) * S::kTile);
       const uint32_t a1 = a0 + S::kTile;
-      const uint32_t out = kColOut + ob * 128;
-      auto issue_st = [&](int u) {
-        const uint32_t kv = kv_base + u / ns, gu = ub + u;
-        const int h = u % ns, s = kv % kStages;
-        if (h == 0) {
-          ptx::mbar_wait(bar + B_B + s, (kv / kStages) & 1);
-          ptx::tc_fence_after();
-        }
-        const uint32_t off = h * 64 * S::kRowBytes;
-        const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
-        const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
-        const uint32_t id = h ? idesc_s1 : idesc_s0;
-        const uint32_t buf = (gu & 1) * 64;
+      const uint32_t kv = c_kv + c_u / ns, gu = c_ub + c_u;
+      const int h = c_u % ns, s = kv % kStages;
+      if (h == 0) {
+        ptx::mbar_wait(bar + B_B + s, (kv / kStages) & 1);
+        ptx::tc_fence_after();
+      }
+      const uint32_t off = h * 64 * S::kRowBytes;
+      const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
+      const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
+      const uint32_t id = h ? idesc_s1 : idesc_s0;
+      const uint32_t buf = (gu & 1) * 64;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
-          ptx::mma_ss_w(tmem + kColS + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
-                        ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
-          ptx::mma_ss_w(tmem + kColP + buf, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
-                        ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
-        }
-        ptx::mma_commit_w(bar + B_S + (gu & 1));
-      };
-      ptx::mbar_wait(bar + B_AF + ab, (ti >> 1) & 1);
-      ptx::tc_fence_after();
-      issue_st(0);
-      if (nsub > 1) issue_st(1);
+      for (int kk = 0; kk < D / 16; ++kk) {
+        // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
+        ptx::mma_ss_w(tmem + kColS + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
+                      ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
+        ptx::mma_ss_w(tmem + kColP + buf, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
+                      ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
+      }
+      ptx::mma_commit_w(bar + B_S + (gu & 1));
+      if (++c_u == ct.nchunks * ns) {
+        c_kv += ct.nchunks;
+        c_ub += ct.nchunks * ns;
+        ++c_ti;
+        c_u = 0;
+        ctile = seek_tile<RANK, KV_STATIONARY>(g, pl, ctile + gridDim.x, num_tiles, ct);
+      }
+    };
+    issue_next();
+    issue_next();
+    uint32_t kv_base = 0, ub = 0, ti = 0;
+    TileCtx<RANK> t;
+    for (unsigned tile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, t); tile < num_tiles;
+         tile = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, t)) {
+      const int nsub = t.nchunks * ns;
+      const int ob = ti & 1;
+      const uint32_t out = kColOut + ob * 128;
       if (ti >= 2) ptx::mbar_wait(bar + B_OE + ob, ((ti >> 1) - 1) & 1);  // outputs drained
+      if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 15);
       for (int u = 0; u < nsub; ++u) {
         const uint32_t kv = kv_base + u / ns, gu = ub + u;
         const int h = u % ns, s = kv % kStages;
@@ -248,10 +277,12 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           }
         }
         if (h == ns - 1) ptx::mma_commit_w(bar + B_E + s);
+        // The tile's outputs are committed BEFORE the cursor may block on the
+        // stationary tiles of tile ti+2, which need this tile's epilogue.
+        if (u == nsub - 1) ptx::mma_commit_w(bar + B_OF + ob);
         if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 12);
-        if (u + 2 < nsub) issue_st(u + 2);
+        issue_next();
       }
-      ptx::mma_commit_w(bar + B_OF + ob);
       kv_base += t.nchunks;
       ub += nsub;
       ++ti;
@@ -264,77 +295,138 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     const int gtid = (warp & 3) * 32 + lane;  // 0..127 within the group
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = g.scale_log2;
+    const bool issuer = KV_STATIONARY ? (gtid == 0) : (threadIdx.x == 0);  // TMA store issuer
     uint32_t ub = 0, ti = 0, it = 0;
     int tr = 0;
     (void)tr;
     const bool tracer = NA_BWD_TRACE_ON && lane == 0 && (warp == 0 || warp == 4);
-    for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      TileCtx<RANK> t;
-      if (!t.init(g, pl, tile, /*inverse=*/KV_STATIONARY)) continue;
-      const int nsub = t.nchunks * ns;
-      const int ob = ti & 1;
-      RowCtx<RANK> r;
-      r.init(g, pl, t, row, /*inverse=*/KV_STATIONARY);
-      float row_lse2 = 0.f, row_d = 0.f;
-      if constexpr (!KV_STATIONARY) {
-        if (r.valid) {
-          const long long tok = r.out_offset(g, t) / g.D;
-          row_lse2 = lse[tok] * kLog2e;
-          row_d = dvec[tok];
-        }
-      }
-      uint32_t mw[4] = {0u, 0u, 0u, 0u};
-      // Partner (query) LSE / D values of a sub-chunk's 64 columns, staged in
-      // smem: thread gtid fetches column gtid & 63 of LSE (gtid < 64) or D.
-      // The fetch for the group's NEXT sub-chunk is issued before computing
-      // the current one, so its global-load latency overlaps that work.
-      auto fetch = [&](int uu) -> float {
-        const int col = gtid & 63, which = gtid >> 6;
-        const int ccol = (uu % ns) * 64 + col;  // column within the chunk
-        float val = 0.f;
-        if (ccol < pl.rows_kv) {
-          int org[3];
-          t.chunk_origin(pl, uu / ns, org);
-          int rem = ccol;
-          bool ok = true;
-          long long tok = 0;
+    // Row (query) values (-LSE * log2(e), D) of a Q-stationary tile, from the
+    // row-vector layout written by the preprocess kernel.
+    auto row_vals = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r, float& nl2, float& d) {
+      nl2 = 0.f;
+      d = 0.f;
+      if (r.valid) {
+        long long i = rv_base(g, t.bh, t.res);
 #pragma unroll
-          for (int a = 2; a >= 0; --a) {
-            if (a >= RANK) continue;
-            const int cc = org[a] + (a == 0 ? rem : rem % pl.ckv[a]);
-            if (a > 0) rem /= pl.ckv[a];
-            ok = ok && cc < t.Lr[a];
-            tok += (long long)(t.r[a] + g.dil[a] * cc) * g.tstride[a];
-          }
-          if (ok) {
-            tok += (long long)t.bh * g.N;
-            val = which == 0 ? lse[tok] * kLog2e : dvec[tok];
-          }
-        }
-        return val;
-      };
-      const int u_first = (int)((grp - ub) & 1u);
-      if constexpr (KV_STATIONARY) {
-        if (u_first < nsub) {
-          vec[(grp * 2 + (it & 1)) * 128 + (gtid >> 6) * 64 + (gtid & 63)] = fetch(u_first);
-          ptx::named_bar_sync(1 + grp, 128);
-        }
+        for (int a = 0; a < RANK; ++a) i += (long long)r.c[a] * g.rv_cs[a];
+        nl2 = rv[i];
+        d = rv[i + g.rv_plane];
       }
+    };
+    // ---- epilogue of a finished tile ----
+    // Runs after this group's FIRST sub-chunk of the next tile (its P is
+    // already with the tensor core), so the MMAs never wait for it.  Every MMA
+    // of the tile is complete once its outputs are final (B_OF), so the tile's
+    // stationary smem tiles are dead: stage the outputs there in the TMA box
+    // layout (same swizzle) and write them with TMA stores (rows past a ragged
+    // class end are clipped by the hardware).  The buffers return to the
+    // producer (B_AE) once the stores have read them (release_store).
+    // KV-stationary: group 0 stages dK (x scale) in the K tile, group 1 dV in
+    // the V tile.  Q-stationary: the groups split dQ's columns in the Q tile.
+    int store_ab = -1;  // issuer: stationary buffer whose store still reads smem
+    auto release_store = [&]() {
+      if (store_ab >= 0) {
+        ptx::bulk_wait_read<0>();
+        ptx::mbar_arrive(bar + B_AE + store_ab);  // stationary tiles reusable
+        store_ab = -1;
+      }
+    };
+    auto epilogue = [&](const TileCtx<RANK>& t, uint32_t tix) {
+      const int ob = tix & 1, ab = tix & 1;
+      ptx::mbar_wait(bar + B_OF + ob, (tix >> 1) & 1);
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 24);
+      ptx::tc_fence_after();
+      uint8_t* stage = smem + S::kA + (2 * ab + (KV_STATIONARY ? grp : 0)) * S::kTile;
+      constexpr int kCols = KV_STATIONARY ? D : D / 2;
+      const int col0 = KV_STATIONARY ? 0 : grp * (D / 2);  // first column this group writes
+      const uint32_t src = kColOut + ob * 128 + (KV_STATIONARY ? grp * D : grp * (D / 2));
+      const float mul = (KV_STATIONARY && grp) ? 1.f : g.scale;
+#pragma unroll
+      for (int c0 = 0; c0 < kCols; c0 += 16) {
+        uint32_t ov[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3]), "=r"(ov[4]), "=r"(ov[5]), "=r"(ov[6]),
+              "=r"(ov[7]), "=r"(ov[8]), "=r"(ov[9]), "=r"(ov[10]), "=r"(ov[11]), "=r"(ov[12]),
+              "=r"(ov[13]), "=r"(ov[14]), "=r"(ov[15])
+            : "r"(trow + src + c0));
+        ptx::tmem_ld_wait();
+        uint32_t pk[8];
+#pragma unroll
+        for (int c = 0; c < 16; c += 2)
+          pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
+        const int chunk = (col0 + c0) / 8;
+        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk, S::kRowBytes)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + 1, S::kRowBytes)) =
+            make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(bar + B_OE + ob);
+      ptx::fence_proxy_async();  // staged tile visible to the TMA engine
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 25);
+      if constexpr (KV_STATIONARY) ptx::named_bar_sync(3 + grp, 128);
+      else ptx::named_bar_sync(3, kCompute);
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 26);
+      if (issuer) {
+        const CUtensorMap* om = (KV_STATIONARY && grp) ? &map_out1 : &map_out0;
+        for (int i = 0; i < pl.q_issues; ++i)
+          t.template store_box<RANK>(om, stage + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
+        ptx::bulk_commit();
+        store_ab = ab;
+      }
+    };
+
+    TileCtx<RANK> t, tp;  // current tile; tile whose epilogue is pending
+    RowCtx<RANK> r;
+    bool pend = false;
+    unsigned tile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, t);
+    if (tile < num_tiles) r.init(g, pl, t, row, /*inverse=*/KV_STATIONARY);
+    float row_nl2 = 0.f, row_d = 0.f;
+    if constexpr (!KV_STATIONARY) {
+      if (tile < num_tiles) row_vals(t, r, row_nl2, row_d);
+    }
+    uint32_t kv_base = 0;
+    while (tile < num_tiles) {
+      const int nsub = t.nchunks * ns;
+      const int u_first = (int)((grp - ub) & 1u);
+      // Next tile: found during this group's last sub-chunk of the tile (so a
+      // Q-stationary tile's row values load while that sub-chunk computes).
+      TileCtx<RANK> tn;
+      RowCtx<RANK> rn;
+      unsigned tile_n = num_tiles;
+      bool tn_known = false;
+      float nrow_nl2 = 0.f, nrow_d = 0.f;
+      uint32_t mw[4] = {0u, 0u, 0u, 0u};
       for (int u = u_first; u < nsub; u += 2, ++it) {
+        if (issuer && u != u_first) release_store();  // previous tile's store has had a sub-chunk to read
         const uint32_t gu = ub + u;
         const int j = u / ns, h = u % ns;
         int org[3];
         t.chunk_origin(pl, j, org);
         r.chunk_mask(pl, org, mw);
         const uint32_t w0 = h ? mw[2] : mw[0], w1 = h ? mw[3] : mw[1];
-        float* cv = vec + (grp * 2 + (it & 1)) * 128;  // [LSE2 x64 | D x64] of this sub-chunk's columns
-        float next_val = 0.f;
-        if constexpr (KV_STATIONARY) {
-          if (u + 2 < nsub) next_val = fetch(u + 2);  // lands while this sub-chunk computes
+        // Partner (query) values of the chunk, TMA-loaded with it:
+        // [-LSE*log2(e) x rows_kv | D x rows_kv]; this sub-chunk's 64 columns.
+        const uint32_t kv = kv_base + j;
+        const float* cl = vec + (kv % kStages) * 256 + h * 64;
+        const float* cd = cl + pl.rows_kv;
+        if (u + 2 >= nsub) {
+          tile_n = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, tn);
+          tn_known = true;
+          if (tile_n < num_tiles) {
+            rn.init(g, pl, tn, row, /*inverse=*/KV_STATIONARY);
+            if constexpr (!KV_STATIONARY) row_vals(tn, rn, nrow_nl2, nrow_d);
+          }
         }
         const uint32_t buf = (gu & 1) * 64;
         if (tracer) NA_TRACE_EV(2 + grp, tr, 19);
         ptx::mbar_wait(bar + B_S + (gu & 1), (gu >> 1) & 1);
+        if constexpr (KV_STATIONARY) {
+          // The chunk's stage is still held (its B_E needs this P), so its
+          // phase is current: the row-vector bytes are visible after this.
+          ptx::mbar_wait(bar + B_B + (kv % kStages), (kv / kStages) & 1);
+        }
         if (tracer) NA_TRACE_EV(2 + grp, tr, 20);
         ptx::tc_fence_after();
         uint32_t pk_p[32], pk_s[32];
@@ -355,11 +447,10 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           for (int c = 0; c < 32; c += 4) {
             float4 nl4, dd4;
             if constexpr (KV_STATIONARY) {
-              nl4 = *reinterpret_cast<const float4*>(cv + 32 * gq + c);
-              dd4 = *reinterpret_cast<const float4*>(cv + 64 + 32 * gq + c);
-              nl4 = make_float4(-nl4.x, -nl4.y, -nl4.z, -nl4.w);
+              nl4 = *reinterpret_cast<const float4*>(cl + 32 * gq + c);
+              dd4 = *reinterpret_cast<const float4*>(cd + 32 * gq + c);
             } else {
-              nl4 = make_float4(-row_lse2, -row_lse2, -row_lse2, -row_lse2);
+              nl4 = make_float4(row_nl2, row_nl2, row_nl2, row_nl2);
               dd4 = make_float4(row_d, row_d, row_d, row_d);
             }
             float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])),
@@ -397,72 +488,41 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar + B_P + (gu & 1));
         if (tracer) NA_TRACE_EV(2 + grp, tr, 21);
-        if constexpr (KV_STATIONARY) {
-          if (u + 2 < nsub) {  // publish the prefetched values for the next sub-chunk
-            vec[(grp * 2 + ((it + 1) & 1)) * 128 + (gtid >> 6) * 64 + (gtid & 63)] = next_val;
-            ptx::named_bar_sync(1 + grp, 128);
-          }
+        if (pend) {  // previous tile's outputs, now that the tensor core has this sub-chunk
+          epilogue(tp, ti - 1);
+          pend = false;
         }
       }
       if (tracer) NA_TRACE_EV(2 + grp, tr, 22);
-      // ---- epilogue (overlaps the next tile's MMAs) ----
-      // Every MMA of the tile is complete once the outputs are final, so the
-      // tile's stationary smem tiles are dead: stage the outputs there in the
-      // TMA box layout (same swizzle) and write them with TMA stores (rows
-      // past a ragged class end are clipped by the hardware).  The buffers
-      // return to the producer (B_AE) once the stores have read them.
-      // KV-stationary: group 0 stages dK (x scale) in the K tile, group 1 dV
-      // in the V tile.  Q-stationary: the groups split dQ's columns in the Q tile.
-      ptx::mbar_wait(bar + B_OF + ob, (ti >> 1) & 1);
-      if (tracer) NA_TRACE_EV(2 + grp, tr, 24);
-      ptx::tc_fence_after();
-      const int ab = ti & 1;
-      uint8_t* stage = smem + S::kA + (2 * ab + (KV_STATIONARY ? grp : 0)) * S::kTile;
-      constexpr int kCols = KV_STATIONARY ? D : D / 2;
-      const int col0 = KV_STATIONARY ? 0 : grp * (D / 2);   // first column this group writes
-      const uint32_t src = kColOut + ob * 128 + (KV_STATIONARY ? grp * D : grp * (D / 2));
-      const float mul = (KV_STATIONARY && grp) ? 1.f : g.scale;
-#pragma unroll
-      for (int c0 = 0; c0 < kCols; c0 += 16) {
-        uint32_t ov[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3]), "=r"(ov[4]), "=r"(ov[5]), "=r"(ov[6]),
-              "=r"(ov[7]), "=r"(ov[8]), "=r"(ov[9]), "=r"(ov[10]), "=r"(ov[11]), "=r"(ov[12]),
-              "=r"(ov[13]), "=r"(ov[14]), "=r"(ov[15])
-            : "r"(trow + src + c0));
-        ptx::tmem_ld_wait();
-        uint32_t pk[8];
-#pragma unroll
-        for (int c = 0; c < 16; c += 2)
-          pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
-        const int chunk = (col0 + c0) / 8;
-        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk, S::kRowBytes)) =
-            make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + 1, S::kRowBytes)) =
-            make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      if (pend) {  // this group had no sub-chunk in the tile
+        epilogue(tp, ti - 1);
+        pend = false;
       }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(bar + B_OE + ob);
-      ptx::fence_proxy_async();  // staged tile visible to the TMA engine
-      if (tracer) NA_TRACE_EV(2 + grp, tr, 25);
-      const bool issuer = KV_STATIONARY ? (gtid == 0) : (threadIdx.x == 0);
-      if constexpr (KV_STATIONARY) ptx::named_bar_sync(3 + grp, 128);
-      else ptx::named_bar_sync(3, kCompute);
-      if (tracer) NA_TRACE_EV(2 + grp, tr, 26);
-      if (issuer) {
-        const CUtensorMap* om = (KV_STATIONARY && grp) ? &map_out1 : &map_out0;
-        for (int i = 0; i < pl.q_issues; ++i)
-          t.template store_box<RANK>(om, stage + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
-        ptx::bulk_commit();
-        ptx::bulk_wait_read<0>();
-        ptx::mbar_arrive(bar + B_AE + ab);  // stationary tiles reusable
-      }
-      if (tracer) NA_TRACE_EV(2 + grp, tr, 23);
+      if (issuer) release_store();
+      tp = t;
+      pend = true;
       ub += nsub;
+      kv_base += t.nchunks;
       ++ti;
+      if (!tn_known) {
+        tile_n = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, tn);
+        if (tile_n < num_tiles) {
+          rn.init(g, pl, tn, row, /*inverse=*/KV_STATIONARY);
+          if constexpr (!KV_STATIONARY) row_vals(tn, rn, nrow_nl2, nrow_d);
+        }
+      }
+      tile = tile_n;
+      t = tn;
+      r = rn;
+      row_nl2 = nrow_nl2;
+      row_d = nrow_d;
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 23);
     }
-    if (KV_STATIONARY ? (gtid == 0) : (threadIdx.x == 0)) ptx::bulk_wait<0>();  // stores done before exit
+    if (pend) epilogue(tp, ti - 1);
+    if (issuer) {
+      release_store();
+      ptx::bulk_wait<0>();  // stores done before exit
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -475,22 +535,22 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
 // dK, dV: key-stationary over the inverse halo.
 template <int RANK, int D, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    fna_dkdv_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, const float* __restrict__ lse,
-                const float* __restrict__ dvec, unsigned num_tiles) {
-  bwd_body<RANK, D, BF16, true>(maps, g, pl, lse, dvec, num_tiles);
+    fna_dkdv_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, const float* __restrict__ rv,
+                unsigned num_tiles) {
+  bwd_body<RANK, D, BF16, true>(maps, g, pl, rv, num_tiles);
 }
 
 // dQ: query-stationary over the forward halo.
 template <int RANK, int D, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    fna_dq_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, const float* __restrict__ lse,
-              const float* __restrict__ dvec, unsigned num_tiles) {
-  bwd_body<RANK, D, BF16, false>(maps, g, pl, lse, dvec, num_tiles);
+    fna_dq_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, const float* __restrict__ rv,
+              unsigned num_tiles) {
+  bwd_body<RANK, D, BF16, false>(maps, g, pl, rv, num_tiles);
 }
 
 template <int RANK, int D, bool BF16>
 cudaError_t launch_both(const Geom& g, const TcPlan& pl, const BwdMaps& mkv, const BwdMaps& mq,
-                        const float* lse, const float* dvec, cudaStream_t st) {
+                        const float* rv, cudaStream_t st) {
   const int smem = BwdSmem<D>::kBytes + 1024;
   auto kdkdv = fna_dkdv_tc<RANK, D, BF16>;
   auto kdq = fna_dq_tc<RANK, D, BF16>;
@@ -506,25 +566,25 @@ cudaError_t launch_both(const Geom& g, const TcPlan& pl, const BwdMaps& mkv, con
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const unsigned grid = (unsigned)(tiles < num_sms() ? tiles : num_sms());
   prof_begin(KID_DKDV_TC, st);
-  kdkdv<<<grid, kThreads, smem, st>>>(mkv, g, pl, lse, dvec, (unsigned)tiles);
+  kdkdv<<<grid, kThreads, smem, st>>>(mkv, g, pl, rv, (unsigned)tiles);
   prof_end(st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   prof_begin(KID_DQ_TC, st);
-  kdq<<<grid, kThreads, smem, st>>>(mq, g, pl, lse, dvec, (unsigned)tiles);
+  kdq<<<grid, kThreads, smem, st>>>(mq, g, pl, rv, (unsigned)tiles);
   prof_end(st);
   return cudaGetLastError();
 }
 
 template <int RANK>
 cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const BwdMaps& mkv, const BwdMaps& mq,
-                    const float* lse, const float* dvec, cudaStream_t st) {
+                    const float* rv, cudaStream_t st) {
   const bool bf = dtype == 2;
   if (g.D == 64)
-    return bf ? launch_both<RANK, 64, true>(g, pl, mkv, mq, lse, dvec, st)
-              : launch_both<RANK, 64, false>(g, pl, mkv, mq, lse, dvec, st);
-  return bf ? launch_both<RANK, 32, true>(g, pl, mkv, mq, lse, dvec, st)
-            : launch_both<RANK, 32, false>(g, pl, mkv, mq, lse, dvec, st);
+    return bf ? launch_both<RANK, 64, true>(g, pl, mkv, mq, rv, st)
+              : launch_both<RANK, 64, false>(g, pl, mkv, mq, rv, st);
+  return bf ? launch_both<RANK, 32, true>(g, pl, mkv, mq, rv, st)
+            : launch_both<RANK, 32, false>(g, pl, mkv, mq, rv, st);
 }
 
 }  // namespace
@@ -534,7 +594,7 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
                    float* Dvec, cudaStream_t st, int* launches) {
   const char* why;
   if (!tc_supported(dtype, g, &why)) return cudaErrorNotSupported;
-  cudaError_t e = bwd_preprocess(dtype, g, o, d_o, Dvec, st);
+  cudaError_t e = bwd_preprocess(dtype, g, o, d_o, lse, Dvec, st);  // row-vector layout
   if (e != cudaSuccess) return e;
   TcPlan pl = make_plan(g, 128);
   // dK/dV kernel: stationary K, V tiles; streamed Q, dO chunks; outputs dK, dV.
@@ -553,11 +613,13 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   if ((e = make_map(&mkv.out1, dtype, g, dv, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
   if ((e = make_map(&mq.out0, dtype, g, dq, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
   mq.out1 = mq.out0;
+  if ((e = make_map_rv(&mkv.rv, g, Dvec, pl.ckv)) != cudaSuccess) return e;
+  mq.rv = mkv.rv;
   *launches = 3;
   switch (g.rank) {
-    case 1: return by_type<1>(dtype, g, pl, mkv, mq, lse, Dvec, st);
-    case 2: return by_type<2>(dtype, g, pl, mkv, mq, lse, Dvec, st);
-    default: return by_type<3>(dtype, g, pl, mkv, mq, lse, Dvec, st);
+    case 1: return by_type<1>(dtype, g, pl, mkv, mq, Dvec, st);
+    case 2: return by_type<2>(dtype, g, pl, mkv, mq, Dvec, st);
+    default: return by_type<3>(dtype, g, pl, mkv, mq, Dvec, st);
   }
 }
 

@@ -18,6 +18,9 @@ TcPlan make_plan(const Geom& g, int tile_rows);
 int num_sms();  // SMs of the current device (cached per device)
 cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base,
                      const int box[3], int box_x);
+// fp32 map over the backward row-vector layout (Geom::rv_*): dims (innermost
+// first) X'_{R-1}, ..., X'_0, plane, BH*nres; box = one chunk x both planes.
+cudaError_t make_map_rv(CUtensorMap* map, const Geom& g, const float* base, const int box[3]);
 
 template <bool BF16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -72,6 +75,7 @@ __device__ __forceinline__ constexpr bool use_poly(int c) {
 template <int RANK>
 struct TileCtx {
   int bh;
+  int res;        // flat residue class (r[0] * dil[1] + r[1]) * dil[2] + r[2]
   int r[3];       // residue per axis
   int Lr[3];      // class size per axis
   int q_origin[3];
@@ -87,6 +91,7 @@ struct TileCtx {
     const uint32_t bhq = fdiv(rest, pl.f_nres);
     uint32_t res = rest - bhq * pl.f_nres.d;
     bh = (int)bhq;
+    this->res = (int)res;
     nchunks = 1;
 #pragma unroll
     for (int a = 2; a >= 0; --a) {
@@ -110,6 +115,10 @@ struct TileCtx {
       } else {
         lo[a] = inv_start(q_origin[a], Lr[a], g.k[a], g.causal[a]);
         hi = inv_end(q_origin[a] + qv[a] - 1, Lr[a], g.k[a], g.causal[a]);
+        // Innermost chunk origins on a multiple of 4: the fp32 row-vector TMA
+        // box must start 16-byte aligned (measured: sm_100a raises an illegal
+        // instruction otherwise, tools/tma_probe.cu).  Extra columns are masked.
+        if (a == RANK - 1) lo[a] &= ~3;
       }
       nch[a] = (hi - lo[a] + pl.ckv[a]) / pl.ckv[a];
       nchunks *= nch[a];
@@ -151,6 +160,20 @@ struct TileCtx {
     }
   }
 
+  // TMA load of the row-vector box (both planes) of the chunk at `org`.
+  template <int R>
+  __device__ __forceinline__ void load_rv(const CUtensorMap* m, void* dst, uint64_t* bar, const int org[3],
+                                          const Geom& g) const {
+    const int bhres = bh * g.nres + res;
+    if constexpr (R == 1) {
+      ptx::tma_load_3d_w(dst, m, bar, org[0], 0, bhres);
+    } else if constexpr (R == 2) {
+      ptx::tma_load_4d_w(dst, m, bar, org[1], org[0], 0, bhres);
+    } else {
+      ptx::tma_load_5d_w(dst, m, bar, org[2], org[1], org[0], 0, bhres);
+    }
+  }
+
   // TMA store of the stationary tile's box (one thread issues).
   template <int R>
   __device__ __forceinline__ void store_box(const CUtensorMap* m, const void* src, int x_off,
@@ -166,6 +189,16 @@ struct TileCtx {
     }
   }
 };
+
+// First tile >= `tile` (stepping by gridDim.x) whose context is valid; fills
+// `t` and returns it, or returns num_tiles when the CTA has none left.
+template <int RANK, bool INVERSE>
+__device__ __forceinline__ unsigned seek_tile(const Geom& g, const TcPlan& pl, unsigned tile, unsigned num_tiles,
+                                              TileCtx<RANK>& t) {
+  for (; tile < num_tiles; tile += gridDim.x)
+    if (t.init(g, pl, tile, INVERSE)) break;
+  return tile;
+}
 
 __device__ __forceinline__ void set_range(uint32_t mw[4], int lo, int hi) {
 #pragma unroll

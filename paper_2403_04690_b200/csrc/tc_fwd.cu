@@ -88,7 +88,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   using S = FwdSmem<D>;
   using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (LDS/STS, not generic LD/ST).
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + B_COUNT);
   const int ns = pl.n_kv > 64 ? 2 : 1;  // sub-chunks per chunk

@@ -75,7 +75,8 @@ TcPlan make_plan(const Geom& g, int tile_rows) {
       const int ax = R - 1;
       // candidate innermost box widths
       for (int split = 1; split <= 4; ++split) {
-        int cx = ceil_div(h[ax], split);
+        // multiple of 4: the fp32 row-vector box's inner extent must be 16 bytes
+        int cx = (ceil_div(h[ax], split) + 3) / 4 * 4;
         if (cx > 128 || cx * g.dil[ax] > 256) continue;
         int ck[3] = {1, 1, 1};
         ck[ax] = cx;
@@ -213,6 +214,33 @@ cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* bas
                    R + 2, const_cast<void*>(base), dims, strides, boxd, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t make_map_rv(CUtensorMap* map, const Geom& g, const float* base, const int box[3]) {
+  EncodeTiled enc = encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const int R = g.rank;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t boxd[5], estr[5];
+  for (int i = 0; i < R; ++i) {  // i = 0 innermost
+    const int a = R - 1 - i;
+    dims[i] = g.rv_lc[a];
+    if (i > 0) strides[i - 1] = (cuuint64_t)g.rv_cs[a] * 4;
+    boxd[i] = (cuuint32_t)box[a];
+    estr[i] = 1;
+  }
+  dims[R] = 2;  // planes: -LSE*log2(e), D
+  strides[R - 1] = (cuuint64_t)g.rv_plane * 4;
+  boxd[R] = 2;
+  estr[R] = 1;
+  dims[R + 1] = (cuuint64_t)g.BH * g.nres;
+  strides[R] = (cuuint64_t)g.rv_plane * 8;
+  boxd[R + 1] = 1;
+  estr[R + 1] = 1;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, R + 2, const_cast<float*>(base), dims, strides, boxd,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 

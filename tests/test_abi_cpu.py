@@ -90,8 +90,14 @@ def test_layout_and_impl_codes(na):
 
 
 def test_workspace_size(na):
+    # max(SIMT D vector BH*N*4, tensor-core row-vector layout BH*nres*2*plane*4)
+    # where plane = prod over axes of ceil(L/dil), innermost padded to 4 (na.h).
     p = P(na, batch=2, heads=3, extent=[7, 5], kernel_size=[3, 3])
-    assert na.na_bwd_workspace_size(p) == 2 * 3 * 35 * 4
+    assert na.na_bwd_workspace_size(p) == 2 * 3 * 1 * 2 * (7 * 8) * 4
+    p = P(na, batch=1, heads=2, extent=[9], kernel_size=[3], dilation=[2])
+    assert na.na_bwd_workspace_size(p) == 2 * 2 * 2 * 8 * 4       # classes of 5 and 4 -> 8
+    p = P(na, batch=1, heads=1, extent=[64], kernel_size=[3])
+    assert na.na_bwd_workspace_size(p) == 2 * 64 * 4
     assert na.na_bwd_workspace_size(P(na, kernel_size=[4])) == 0
 
 

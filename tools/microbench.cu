@@ -150,7 +150,11 @@ __global__ void k_ffma2(unsigned long long* out, int iters, int nwarps, float* s
 
 // Back-to-back MMAs (M=128, N=64, K=16, SS, fp16) from one warp; smem operands
 // are whatever smem holds (values irrelevant).  Measures issue + execution.
-__global__ void k_mma(unsigned long long* out, int iters, int n) {
+// mode 0: SS, B K-major; mode 1: SS, B MN-major; mode 2: TS (A in TMEM cols
+// 128..), B MN-major; mode 3: TS, B K-major.
+template <int MODE, int N>
+__global__ void k_mma(unsigned long long* out, int iters) {
+  constexpr int mode = MODE, n = N;
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
@@ -164,15 +168,21 @@ __global__ void k_mma(unsigned long long* out, int iters, int n) {
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t a = ptx::smem_u32(sm), b = a + 16384;
-  const uint32_t idesc = ptx::make_idesc(128, n, false, false);
+  constexpr bool bmn = mode == 1 || mode == 2;
+  constexpr uint32_t idesc = ptx::make_idesc(128, n, false, bmn);
   unsigned long long t0 = 0, t1 = 0;
   if (warp == 0) {
     t0 = clock64();
     for (int i = 0; i < iters; ++i) {
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        ptx::mma_ss_w(slot, ptx::make_sdesc(a + kk * 32, 16, 1024, 2), ptx::make_sdesc(b + kk * 32, 16, 1024, 2),
-                      idesc, 1u);
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t bd = bmn ? ptx::make_sdesc(b + kk * 16 * 128, 128 * 128, 1024, 2)
+                                : ptx::make_sdesc(b + kk * 32, 16, 1024, 2);
+        if constexpr (mode >= 2)
+          ptx::mma_ts_w(slot, slot + 128 + kk * 8, bd, idesc, 1u);
+        else
+          ptx::mma_ss_w(slot, ptx::make_sdesc(a + kk * 32, 16, 1024, 2), bd, idesc, 1u);
+      }
     }
     ptx::mma_commit_w(&bar);
     ptx::mbar_wait(&bar, 0);
@@ -226,14 +236,23 @@ int main() {
     const double cf = avg(h, sms);
     printf("ffma2 warps=%2d: %.1f fp32 FMA/clk/SM\n", nw, nw * 32.0 * 16 * iters / cf);
   }
-  cudaFuncSetAttribute(k_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-  for (int n : {64, 128, 256}) {
-    k_mma<<<sms, 128, 65536>>>(d, 200, n);
+  auto run = [&](auto kern, const char* name, int n) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    kern<<<sms, 128, 65536>>>(d, 200);
     cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
     const double cyc = avg(h, sms);
-    printf("mma   M128 N%-3d K16: %.1f clk/MMA  -> %.0f flop/clk/SM\n", n, cyc / (200 * 4),
+    printf("mma %s M128 N%-3d K16: %.1f clk/MMA  -> %.0f flop/clk/SM\n", name, n, cyc / (200 * 4),
            2.0 * 128 * n * 16 * 200 * 4 / cyc);
-  }
+  };
+  run(k_mma<0, 64>, "SS Bk ", 64);
+  run(k_mma<0, 128>, "SS Bk ", 128);
+  run(k_mma<0, 256>, "SS Bk ", 256);
+  run(k_mma<1, 64>, "SS Bmn", 64);
+  run(k_mma<1, 128>, "SS Bmn", 128);
+  run(k_mma<2, 64>, "TS Bmn", 64);
+  run(k_mma<2, 128>, "TS Bmn", 128);
+  run(k_mma<3, 64>, "TS Bk ", 64);
+  run(k_mma<3, 128>, "TS Bk ", 128);
   cudaError_t e = cudaDeviceSynchronize();
   printf("status: %s\n", cudaGetErrorString(e));
   return 0;

@@ -46,11 +46,15 @@ t = buf.view(64, 4, 256).cpu()
 import collections
 for cta in (0, 37):
     print(f"--- CTA {cta}")
+    allev = [[((x >> 8), x & 0xFF) for x in t[cta, role].tolist() if x != 0] for role in range(4)]
+    t0 = min(e[0][0] for e in allev if e)  # one clock origin for every role of the CTA
+    merged = sorted((c, role, tag) for role, e in enumerate(allev) for c, tag in e)
+    tmax = merged[0][0] + 60000
+    print("  merged (cycle:role.tag): " + "  ".join(f"{c - t0}:{r}.{tag}" for c, r, tag in merged if c < tmax))
     for role in range(4):
-        evs = [((x >> 8), x & 0xFF) for x in t[cta, role].tolist() if x != 0]
+        evs = allev[role]
         if not evs:
             continue
-        t0 = evs[0][0]
         print(f"  role {role}: " + "  ".join(f"{c - t0}:{tag}" for c, tag in evs[:40]))
         by = collections.defaultdict(list)
         for i2 in range(1, len(evs)):
