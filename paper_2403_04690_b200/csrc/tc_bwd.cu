@@ -44,13 +44,14 @@ static __device__ int g_trace_sel;  // trace build: 1 = dK/dV kernel, 0 = dQ ker
 #define NA_BWD_TRACE_ON false
 #endif
 
-constexpr int kStages = 2;
-constexpr int kThreads = 320;
+constexpr int kStages = 4;
+constexpr int kThreads = 352;
 constexpr int kCompute = 256;  // compute threads (warps 0..7)
 // The warp scheduler favours the highest warp id among eligible warps, so the
 // latency-critical single-lane roles take the highest ids.
 constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
+constexpr int kMmaWarp = 9;    // TMEM owner; OUT MMAs (dV, dK | dQ), in sub-chunk order
+constexpr int kSWarp = 10;     // S / dP MMAs, as far ahead as the TMEM buffers allow
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
@@ -65,20 +66,25 @@ struct BwdSmem {
   static constexpr int kBytes = kBar + 256;
 };
 
-// TMEM columns: [0,128) two 64-column S-like buffers, [128,256) two dP-like
-// buffers, [256 + 128*ob, ...) output accumulators of tile parity ob
-// (first output at +0, second at +D).
-constexpr uint32_t kColS = 0, kColP = 128, kColOut = 256;
+// TMEM columns (512): [0,128) two 64-column S buffers and [128,256) two dP
+// buffers, each released (B_SF) as soon as its warpgroup has loaded it, so the
+// MMAs of the sub-chunk two ahead overlap this one's softmax; [256,384) two
+// packed-operand buffers (16-bit pairs: P^T at +0, dS^T at +32; dQ: dS at
+// +0), read by the OUT MMAs; [384,512) output accumulators: dK | dV (2D
+// columns, single-buffered when 2D = 128) or dQ (D columns, double-buffered).
+constexpr uint32_t kColS = 0, kColP = 128, kColPk = 256, kColOut = 384;
 
 enum : int {
   B_AF = 0,                 // stationary tiles full [2]
-  B_AE = B_AF + 2,          // stationary tiles empty [2]
+  B_AE = B_AF + 2,          // stationary tiles empty [2] (the TMA-store issuer, after the read)
   B_B = B_AE + 2,           // streamed stage full [kStages]
   B_E = B_B + kStages,      // streamed stage empty [kStages]
   B_S = B_E + kStages,      // S and dP of a sub-chunk ready [2]
-  B_P = B_S + 2,            // packed operands of a sub-chunk written [2] (128 arrivals)
-  B_OF = B_P + 2,           // outputs of a tile final [2]
-  B_OE = B_OF + 2,          // outputs drained by the epilogue [2] (256 arrivals)
+  B_SF = B_S + 2,           // S and dP buffers loaded by the warpgroup [2] (128 arrivals)
+  B_P = B_SF + 2,           // packed operands written [2] (128 arrivals)
+  B_PE = B_P + 2,           // packed operands consumed by the OUT MMAs [2]
+  B_OF = B_PE + 2,          // outputs of a tile final [2]
+  B_OE = B_OF + 2,          // outputs drained [2]
   B_COUNT = B_OE + 2
 };
 
@@ -99,7 +105,9 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   const CUtensorMap& map_out0 = maps.out0;
   const CUtensorMap& map_out1 = maps.out1;
   using S = BwdSmem<D>;
-  using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
+  // Output accumulator columns per tile; double-buffered when two fit.
+  constexpr int kOutCols = KV_STATIONARY ? 2 * D : D;
+  constexpr bool kOutDouble = 2 * kOutCols <= 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared address space (LDS/STS, not generic LD/ST).
@@ -113,11 +121,13 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(bar + B_AF + b, 1);
-      ptx::mbar_init(bar + B_AE + b, KV_STATIONARY ? 2 : 1);  // released by the store issuers
+      ptx::mbar_init(bar + B_AE + b, 1);
       ptx::mbar_init(bar + B_S + b, 1);
+      ptx::mbar_init(bar + B_SF + b, 128);
       ptx::mbar_init(bar + B_P + b, 128);
+      ptx::mbar_init(bar + B_PE + b, 1);
       ptx::mbar_init(bar + B_OF + b, 1);
-      ptx::mbar_init(bar + B_OE + b, kCompute);
+      ptx::mbar_init(bar + B_OE + b, KV_STATIONARY ? 128 : kCompute);
     }
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(bar + B_B + s, 1);
@@ -184,108 +194,109 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       }
       ++ti;
     }
-  } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (whole warp, one lane issues) =====================
+  } else if (warp == kMmaWarp || warp == kSWarp) {
+    // ============ MMA issuers (whole warps, one elected lane issues) ============
+    // Two independent in-order streams, so neither blocks the other: warp
+    // kSWarp issues S/dP of sub-chunk c once its TMEM buffer is free (B_SF of
+    // c-2) and its operands are resident; warp kMmaWarp issues OUT(k) once
+    // sub-chunk k's packed operands are written.  A commit tracks the MMAs of
+    // its own issuing thread: B_S (S warp); B_PE, B_E, B_OF (OUT warp) -- the
+    // S/dP MMAs of a chunk are complete before its last OUT is issued (the
+    // warpgroup read their results first), so B_E covers both.
     constexpr uint32_t kSw = D == 64 ? 2u : 4u;
     constexpr uint32_t kSbo = 8 * S::kRowBytes;
-    const int n1 = pl.n_kv - 64;
-    const uint32_t idesc_s0 = ptx::make_idesc(128, ns == 2 ? 64 : pl.n_kv, BF16, false);
-    const uint32_t idesc_s1 = ptx::make_idesc(128, ns == 2 ? n1 : 16, BF16, false);
-    constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
     int tr = 0;
     (void)tr;
-    // Issue cursor: the S/dP MMAs of sub-chunk (tile, u) run two sub-chunks
-    // ahead of the OUT MMAs, ACROSS tile boundaries, so the next tile's first
-    // sub-chunks are computed while this tile's last ones are consumed.
-    TileCtx<RANK> ct;
-    unsigned ctile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, ct);
-    uint32_t c_ti = 0, c_kv = 0, c_ub = 0;
-    int c_u = 0;
-    auto issue_next = [&]() {
-      if (ctile >= num_tiles) return;
-      const int ab = c_ti & 1;
-      if (c_u == 0) {
-        ptx::mbar_wait(bar + B_AF + ab, (c_ti >> 1) & 1);
-        if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 14);
-        ptx::tc_fence_after();
-      }
-      const uint32_t a0 = ptx::smem_u32(smem + S::kA + (2 * ab) * S::kTile);
-      const uint32_t a1 = a0 + S::kTile;
-      const uint32_t kv = c_kv + c_u / ns, gu = c_ub + c_u;
-      const int h = c_u % ns, s = kv % kStages;
-      if (h == 0) {
-        ptx::mbar_wait(bar + B_B + s, (kv / kStages) & 1);
-        ptx::tc_fence_after();
-      }
-      const uint32_t off = h * 64 * S::kRowBytes;
-      const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
-      const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
-      const uint32_t id = h ? idesc_s1 : idesc_s0;
-      const uint32_t buf = (gu & 1) * 64;
+    if (warp == kSWarp) {
+      const int n1 = pl.n_kv - 64;
+      const uint32_t idesc_s0 = ptx::make_idesc(128, ns == 2 ? 64 : pl.n_kv, BF16, false);
+      const uint32_t idesc_s1 = ptx::make_idesc(128, ns == 2 ? n1 : 16, BF16, false);
+      uint32_t c_ti = 0, c_kv = 0, c_ub = 0;
+      TileCtx<RANK> ct;
+      for (unsigned tile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, ct); tile < num_tiles;
+           tile = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, ct)) {
+        const int ab = c_ti & 1;
+        const uint32_t a0 = ptx::smem_u32(smem + S::kA + (2 * ab) * S::kTile);
+        const uint32_t a1 = a0 + S::kTile;
+        const int nsub = ct.nchunks * ns;
+        for (int c_u = 0; c_u < nsub; ++c_u) {
+          const uint32_t kv = c_kv + c_u / ns, gu = c_ub + c_u;
+          const int h = c_u % ns, s = kv % kStages;
+          if (gu >= 2) ptx::mbar_wait(bar + B_SF + (gu & 1), ((gu >> 1) - 1) & 1);  // buffer loaded
+          if (c_u == 0) ptx::mbar_wait(bar + B_AF + ab, (c_ti >> 1) & 1);
+          if (h == 0) ptx::mbar_wait(bar + B_B + s, (kv / kStages) & 1);
+          ptx::tc_fence_after();
+          const uint32_t off = h * 64 * S::kRowBytes;
+          const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
+          const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
+          const uint32_t id = h ? idesc_s1 : idesc_s0;
+          const uint32_t buf = (gu & 1) * 64;
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
-        ptx::mma_ss_w(tmem + kColS + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
-                      ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
-        ptx::mma_ss_w(tmem + kColP + buf, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
-                      ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
-      }
-      ptx::mma_commit_w(bar + B_S + (gu & 1));
-      if (++c_u == ct.nchunks * ns) {
-        c_kv += ct.nchunks;
-        c_ub += ct.nchunks * ns;
-        ++c_ti;
-        c_u = 0;
-        ctile = seek_tile<RANK, KV_STATIONARY>(g, pl, ctile + gridDim.x, num_tiles, ct);
-      }
-    };
-    issue_next();
-    issue_next();
-    uint32_t kv_base = 0, ub = 0, ti = 0;
-    TileCtx<RANK> t;
-    for (unsigned tile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, t); tile < num_tiles;
-         tile = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, t)) {
-      const int nsub = t.nchunks * ns;
-      const int ob = ti & 1;
-      const uint32_t out = kColOut + ob * 128;
-      if (ti >= 2) ptx::mbar_wait(bar + B_OE + ob, ((ti >> 1) - 1) & 1);  // outputs drained
-      if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 15);
-      for (int u = 0; u < nsub; ++u) {
-        const uint32_t kv = kv_base + u / ns, gu = ub + u;
-        const int h = u % ns, s = kv % kStages;
-        const int width = h ? n1 : (ns == 2 ? 64 : pl.n_kv);
-        const uint32_t off = h * 64 * S::kRowBytes;
-        const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
-        const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
-        const uint32_t buf = (gu & 1) * 64;
-        ptx::mbar_wait(bar + B_P + (gu & 1), (gu >> 1) & 1);
-        if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 11);
-        ptx::tc_fence_after();
-        for (int kk = 0; kk < width / 16; ++kk) {
-          const uint32_t boff = kk * 16 * S::kRowBytes;
-          const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
-          if constexpr (KV_STATIONARY) {
-            // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
-            ptx::mma_ts_w(tmem + out + D, tmem + kColS + buf + kk * 8,
-                          ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
-            ptx::mma_ts_w(tmem + out, tmem + kColP + buf + kk * 8,
-                          ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
-          } else {
-            // dQ += dS K
-            ptx::mma_ts_w(tmem + out, tmem + kColS + buf + kk * 8,
-                          ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
+            ptx::mma_ss_w(tmem + kColS + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
+                          ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
+            ptx::mma_ss_w(tmem + kColP + buf, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
+                          ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
           }
+          ptx::mma_commit_w(bar + B_S + (gu & 1));
         }
-        if (h == ns - 1) ptx::mma_commit_w(bar + B_E + s);
-        // The tile's outputs are committed BEFORE the cursor may block on the
-        // stationary tiles of tile ti+2, which need this tile's epilogue.
-        if (u == nsub - 1) ptx::mma_commit_w(bar + B_OF + ob);
-        if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 12);
-        issue_next();
+        c_kv += ct.nchunks;
+        c_ub += nsub;
+        ++c_ti;
       }
-      kv_base += t.nchunks;
-      ub += nsub;
-      ++ti;
+    } else {
+      const int n1 = pl.n_kv - 64;
+      constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
+      uint32_t kv_base = 0, ub = 0, ti = 0;
+      TileCtx<RANK> t;
+      for (unsigned tile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, t); tile < num_tiles;
+           tile = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, t)) {
+        const int nsub = t.nchunks * ns;
+        const int ob = kOutDouble ? (ti & 1) : 0;
+        const uint32_t out = kColOut + ob * kOutCols;
+        for (int u = 0; u < nsub; ++u) {
+          const uint32_t kv = kv_base + u / ns, gu = ub + u;
+          const int h = u % ns, s = kv % kStages;
+          const int width = h ? n1 : (ns == 2 ? 64 : pl.n_kv);
+          const uint32_t off = h * 64 * S::kRowBytes;
+          const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
+          const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
+          const uint32_t pk = tmem + kColPk + (gu & 1) * 64;
+          ptx::mbar_wait(bar + B_P + (gu & 1), (gu >> 1) & 1);
+          if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 11);
+          if (u == 0) {  // the tile's first OUT MMA overwrites the output buffer: drained?
+            if (kOutDouble) {
+              if (ti >= 2) ptx::mbar_wait(bar + B_OE + ob, ((ti >> 1) - 1) & 1);
+            } else {
+              if (ti >= 1) ptx::mbar_wait(bar + B_OE, (ti - 1) & 1);
+            }
+          }
+          ptx::tc_fence_after();
+          for (int kk = 0; kk < width / 16; ++kk) {
+            const uint32_t boff = kk * 16 * S::kRowBytes;
+            const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
+            if constexpr (KV_STATIONARY) {
+              // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
+              ptx::mma_ts_w(tmem + out + D, pk + kk * 8,
+                            ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+              ptx::mma_ts_w(tmem + out, pk + 32 + kk * 8,
+                            ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+            } else {
+              // dQ += dS K
+              ptx::mma_ts_w(tmem + out, pk + kk * 8,
+                            ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+            }
+          }
+          ptx::mma_commit_w(bar + B_PE + (gu & 1));
+          if (h == ns - 1) ptx::mma_commit_w(bar + B_E + s);
+          if (u == nsub - 1) ptx::mma_commit_w(bar + B_OF + ob);
+          if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 12);
+        }
+        kv_base += t.nchunks;
+        ub += nsub;
+        ++ti;
+      }
     }
   } else {
     // ===================== compute warpgroups (2 x 128 threads) =====================
@@ -295,8 +306,9 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     const int gtid = (warp & 3) * 32 + lane;  // 0..127 within the group
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = g.scale_log2;
-    const bool issuer = KV_STATIONARY ? (gtid == 0) : (threadIdx.x == 0);  // TMA store issuer
-    uint32_t ub = 0, ti = 0, it = 0;
+    // TMA-store issuer: dK/dV, thread 0 of the draining group; dQ, thread 0.
+    const bool issuer = KV_STATIONARY ? (gtid == 0) : (threadIdx.x == 0);
+    uint32_t ub = 0, ti = 0;
     int tr = 0;
     (void)tr;
     const bool tracer = NA_BWD_TRACE_ON && lane == 0 && (warp == 0 || warp == 4);
@@ -314,15 +326,17 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       }
     };
     // ---- epilogue of a finished tile ----
-    // Runs after this group's FIRST sub-chunk of the next tile (its P is
-    // already with the tensor core), so the MMAs never wait for it.  Every MMA
-    // of the tile is complete once its outputs are final (B_OF), so the tile's
-    // stationary smem tiles are dead: stage the outputs there in the TMA box
-    // layout (same swizzle) and write them with TMA stores (rows past a ragged
-    // class end are clipped by the hardware).  The buffers return to the
-    // producer (B_AE) once the stores have read them (release_store).
-    // KV-stationary: group 0 stages dK (x scale) in the K tile, group 1 dV in
-    // the V tile.  Q-stationary: the groups split dQ's columns in the Q tile.
+    // Every MMA of the tile is complete once its outputs are final (B_OF), so
+    // the tile's stationary smem tiles are dead: the outputs are staged there
+    // in the TMA box layout (same swizzle) and written with TMA stores (rows
+    // past a ragged class end are clipped by the hardware).  The buffers
+    // return to the producer (B_AE) once the stores have read them
+    // (release_store, deferred to the issuer's next sub-chunk or tile end).
+    // dK/dV (single output buffer): at the start of the next tile, ONE group
+    // (the one not owning its first sub-chunk) drains dK (x scale) into the K
+    // tile and dV into the V tile, while the other computes.  dQ (double
+    // buffer): after each group's first sub-chunk of the next tile, the
+    // groups drain one half of dQ's columns each.
     int store_ab = -1;  // issuer: stationary buffer whose store still reads smem
     auto release_store = [&]() {
       if (store_ab >= 0) {
@@ -331,18 +345,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         store_ab = -1;
       }
     };
-    auto epilogue = [&](const TileCtx<RANK>& t, uint32_t tix) {
-      const int ob = tix & 1, ab = tix & 1;
-      ptx::mbar_wait(bar + B_OF + ob, (tix >> 1) & 1);
-      if (tracer) NA_TRACE_EV(2 + grp, tr, 24);
-      ptx::tc_fence_after();
-      uint8_t* stage = smem + S::kA + (2 * ab + (KV_STATIONARY ? grp : 0)) * S::kTile;
-      constexpr int kCols = KV_STATIONARY ? D : D / 2;
-      const int col0 = KV_STATIONARY ? 0 : grp * (D / 2);  // first column this group writes
-      const uint32_t src = kColOut + ob * 128 + (KV_STATIONARY ? grp * D : grp * (D / 2));
-      const float mul = (KV_STATIONARY && grp) ? 1.f : g.scale;
-#pragma unroll
-      for (int c0 = 0; c0 < kCols; c0 += 16) {
+    auto drain = [&](uint32_t src, uint8_t* stage, int col0, int ncols, float mul) {
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
         uint32_t ov[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -361,17 +365,33 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + 1, S::kRowBytes)) =
             make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
+    };
+    auto epilogue = [&](const TileCtx<RANK>& t, uint32_t tix) {
+      const int ob = kOutDouble ? (tix & 1) : 0, ab = tix & 1;
+      ptx::mbar_wait(bar + B_OF + ob, kOutDouble ? ((tix >> 1) & 1) : (tix & 1));
+      if (tracer) NA_TRACE_EV(2 + grp, tr, 24);
+      ptx::tc_fence_after();
+      uint8_t* stage0 = smem + S::kA + (2 * ab) * S::kTile;
+      const uint32_t src = kColOut + ob * kOutCols;
+      if constexpr (KV_STATIONARY) {
+        drain(src, stage0, 0, D, g.scale);                 // dK -> K tile
+        drain(src + D, stage0 + S::kTile, 0, D, 1.f);      // dV -> V tile
+      } else {
+        drain(src + grp * (D / 2), stage0, grp * (D / 2), D / 2, g.scale);  // half of dQ -> Q tile
+      }
       ptx::tc_fence_before();
       ptx::mbar_arrive(bar + B_OE + ob);
       ptx::fence_proxy_async();  // staged tile visible to the TMA engine
       if (tracer) NA_TRACE_EV(2 + grp, tr, 25);
       if constexpr (KV_STATIONARY) ptx::named_bar_sync(3 + grp, 128);
       else ptx::named_bar_sync(3, kCompute);
-      if (tracer) NA_TRACE_EV(2 + grp, tr, 26);
       if (issuer) {
-        const CUtensorMap* om = (KV_STATIONARY && grp) ? &map_out1 : &map_out0;
-        for (int i = 0; i < pl.q_issues; ++i)
-          t.template store_box<RANK>(om, stage + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
+        for (int i = 0; i < pl.q_issues; ++i) {
+          t.template store_box<RANK>(&map_out0, stage0 + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
+          if constexpr (KV_STATIONARY)
+            t.template store_box<RANK>(&map_out1, stage0 + S::kTile + i * pl.q_box_x * S::kRowBytes,
+                                       i * pl.q_box_x, g);
+        }
         ptx::bulk_commit();
         store_ab = ab;
       }
@@ -390,6 +410,11 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     while (tile < num_tiles) {
       const int nsub = t.nchunks * ns;
       const int u_first = (int)((grp - ub) & 1u);
+      if constexpr (KV_STATIONARY) {
+        // The group not owning the tile's first sub-chunk drains the previous tile.
+        if (pend && u_first == 1) epilogue(tp, ti - 1);
+        pend = false;
+      }
       // Next tile: found during this group's last sub-chunk of the tile (so a
       // Q-stationary tile's row values load while that sub-chunk computes).
       TileCtx<RANK> tn;
@@ -398,14 +423,14 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       bool tn_known = false;
       float nrow_nl2 = 0.f, nrow_d = 0.f;
       uint32_t mw[4] = {0u, 0u, 0u, 0u};
-      for (int u = u_first; u < nsub; u += 2, ++it) {
-        if (issuer && u != u_first) release_store();  // previous tile's store has had a sub-chunk to read
+      for (int u = u_first; u < nsub; u += 2) {
+        if (issuer && u != u_first) release_store();  // the store has had a sub-chunk to read
         const uint32_t gu = ub + u;
         const int j = u / ns, h = u % ns;
         int org[3];
         t.chunk_origin(pl, j, org);
         r.chunk_mask(pl, org, mw);
-        const uint32_t w0 = h ? mw[2] : mw[0], w1 = h ? mw[3] : mw[1];
+        const uint32_t w[2] = {h ? mw[2] : mw[0], h ? mw[3] : mw[1]};
         // Partner (query) values of the chunk, TMA-loaded with it:
         // [-LSE*log2(e) x rows_kv | D x rows_kv]; this sub-chunk's 64 columns.
         const uint32_t kv = kv_base + j;
@@ -429,74 +454,91 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         }
         if (tracer) NA_TRACE_EV(2 + grp, tr, 20);
         ptx::tc_fence_after();
-        uint32_t pk_p[32], pk_s[32];
+        // Per 32-column half: load S and dP; after the second half's load the
+        // S/dP buffer is released (B_SF) so the sub-chunk two ahead can start.
+        const uint32_t pk = trow + kColPk + buf;
+        uint32_t pk_p[2][16], pk_s[2][16];
 #pragma unroll
         for (int gq = 0; gq < 2; ++gq) {
-          const uint32_t w = gq ? w1 : w0;
-          if (!__any_sync(0xffffffffu, w != 0u)) {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) pk_p[16 * gq + c] = pk_s[16 * gq + c] = 0u;
-            continue;
-          }
-          const bool full = __all_sync(0xffffffffu, w == 0xffffffffu);
+          const bool any = __any_sync(0xffffffffu, w[gq] != 0u);
           uint32_t sv[32], pv[32];
-          NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
-          NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 32; c += 4) {
-            float4 nl4, dd4;
-            if constexpr (KV_STATIONARY) {
-              nl4 = *reinterpret_cast<const float4*>(cl + 32 * gq + c);
-              dd4 = *reinterpret_cast<const float4*>(cd + 32 * gq + c);
-            } else {
-              nl4 = make_float4(row_nl2, row_nl2, row_nl2, row_nl2);
-              dd4 = make_float4(row_d, row_d, row_d, row_d);
-            }
-            float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])),
-                                   make_float2(sl2, sl2), make_float2(nl4.x, nl4.y));
-            float2 x1 = __ffma2_rn(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])),
-                                   make_float2(sl2, sl2), make_float2(nl4.z, nl4.w));
-            if (!full) {
-              x0.x = (w >> c) & 1u ? x0.x : -INFINITY;
-              x0.y = (w >> (c + 1)) & 1u ? x0.y : -INFINITY;
-              x1.x = (w >> (c + 2)) & 1u ? x1.x : -INFINITY;
-              x1.y = (w >> (c + 3)) & 1u ? x1.y : -INFINITY;
-            }
-            const float2 p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
-            const float2 p1 = use_poly(c) ? exp2_poly2(x1)                   // FMA pipe
-                                          : make_float2(ptx::ex2(x1.x), ptx::ex2(x1.y));
-            const float2 ds0 = __fmul2_rn(p0, __fadd2_rn(make_float2(__uint_as_float(pv[c]),
-                                                                     __uint_as_float(pv[c + 1])),
-                                                         make_float2(-dd4.x, -dd4.y)));
-            const float2 ds1 = __fmul2_rn(p1, __fadd2_rn(make_float2(__uint_as_float(pv[c + 2]),
-                                                                     __uint_as_float(pv[c + 3])),
-                                                         make_float2(-dd4.z, -dd4.w)));
-            pk_p[16 * gq + (c >> 1)] = pack2<BF16>(p0.x, p0.y);
-            pk_p[16 * gq + (c >> 1) + 1] = pack2<BF16>(p1.x, p1.y);
-            pk_s[16 * gq + (c >> 1)] = pack2<BF16>(ds0.x, ds0.y);
-            pk_s[16 * gq + (c >> 1) + 1] = pack2<BF16>(ds1.x, ds1.y);
+          if (any) {
+            NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
+            NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
+            ptx::tmem_ld_wait();
           }
-        }
-        if constexpr (KV_STATIONARY) {
-          NA_TMEM_ST32(trow + kColS + buf, pk_p);  // P^T  -> A of dV += P^T dO
-          NA_TMEM_ST32(trow + kColP + buf, pk_s);  // dS^T -> A of dK += dS^T Q
-        } else {
-          NA_TMEM_ST32(trow + kColS + buf, pk_s);  // dS -> A of dQ += dS K
+          if (gq == 1) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(bar + B_SF + (gu & 1));
+          } else if (gu >= 2) {
+            ptx::mbar_wait(bar + B_PE + (gu & 1), ((gu >> 1) - 1) & 1);  // packed buffer free
+            ptx::tc_fence_after();
+          }
+          if (!any) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) pk_p[gq][c] = pk_s[gq][c] = 0u;
+          } else {
+            const bool full = __all_sync(0xffffffffu, w[gq] == 0xffffffffu);
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+              float4 nl4, dd4;
+              if constexpr (KV_STATIONARY) {
+                nl4 = *reinterpret_cast<const float4*>(cl + 32 * gq + c);
+                dd4 = *reinterpret_cast<const float4*>(cd + 32 * gq + c);
+              } else {
+                nl4 = make_float4(row_nl2, row_nl2, row_nl2, row_nl2);
+                dd4 = make_float4(row_d, row_d, row_d, row_d);
+              }
+              float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])),
+                                     make_float2(sl2, sl2), make_float2(nl4.x, nl4.y));
+              float2 x1 = __ffma2_rn(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])),
+                                     make_float2(sl2, sl2), make_float2(nl4.z, nl4.w));
+              if (!full) {
+                const uint32_t ww = w[gq];
+                x0.x = (ww >> c) & 1u ? x0.x : -INFINITY;
+                x0.y = (ww >> (c + 1)) & 1u ? x0.y : -INFINITY;
+                x1.x = (ww >> (c + 2)) & 1u ? x1.x : -INFINITY;
+                x1.y = (ww >> (c + 3)) & 1u ? x1.y : -INFINITY;
+              }
+              const float2 p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
+              const float2 p1 = use_poly(c) ? exp2_poly2(x1)                   // FMA pipe
+                                            : make_float2(ptx::ex2(x1.x), ptx::ex2(x1.y));
+              const float2 ds0 = __fmul2_rn(
+                  p0, __fadd2_rn(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])),
+                                 make_float2(-dd4.x, -dd4.y)));
+              const float2 ds1 = __fmul2_rn(
+                  p1, __fadd2_rn(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])),
+                                 make_float2(-dd4.z, -dd4.w)));
+              pk_p[gq][c >> 1] = pack2<BF16>(p0.x, p0.y);
+              pk_p[gq][(c >> 1) + 1] = pack2<BF16>(p1.x, p1.y);
+              pk_s[gq][c >> 1] = pack2<BF16>(ds0.x, ds0.y);
+              pk_s[gq][(c >> 1) + 1] = pack2<BF16>(ds1.x, ds1.y);
+            }
+          }
+          if constexpr (KV_STATIONARY) {
+            NA_TMEM_ST16(pk + 16 * gq, pk_p[gq]);       // P^T  -> A of dV += P^T dO
+            NA_TMEM_ST16(pk + 32 + 16 * gq, pk_s[gq]);  // dS^T -> A of dK += dS^T Q
+          } else {
+            NA_TMEM_ST16(pk + 16 * gq, pk_s[gq]);       // dS -> A of dQ += dS K
+          }
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar + B_P + (gu & 1));
         if (tracer) NA_TRACE_EV(2 + grp, tr, 21);
-        if (pend) {  // previous tile's outputs, now that the tensor core has this sub-chunk
-          epilogue(tp, ti - 1);
-          pend = false;
+        if constexpr (!KV_STATIONARY) {
+          if (pend) {  // previous tile's dQ, now that the tensor core has this sub-chunk
+            epilogue(tp, ti - 1);
+            pend = false;
+          }
         }
       }
       if (tracer) NA_TRACE_EV(2 + grp, tr, 22);
-      if (pend) {  // this group had no sub-chunk in the tile
-        epilogue(tp, ti - 1);
-        pend = false;
+      if constexpr (!KV_STATIONARY) {
+        if (pend) {  // this group had no sub-chunk in the tile
+          epilogue(tp, ti - 1);
+          pend = false;
+        }
       }
       if (issuer) release_store();
       tp = t;
@@ -518,7 +560,13 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       row_d = nrow_d;
       if (tracer) NA_TRACE_EV(2 + grp, tr, 23);
     }
-    if (pend) epilogue(tp, ti - 1);
+    if (pend) {
+      if constexpr (KV_STATIONARY) {
+        if ((int)((grp - ub) & 1u) == 1) epilogue(tp, ti - 1);
+      } else {
+        epilogue(tp, ti - 1);
+      }
+    }
     if (issuer) {
       release_store();
       ptx::bulk_wait<0>();  // stores done before exit
