@@ -16,14 +16,18 @@
 //   fna_dq_tc    query-stationary over the forward halo: S = Q K^T, dP = dO V^T,
 //                dS = P (dP - D), dQ += dS K.
 // Persistent, 1 CTA per SM walking tiles blockIdx.x, +gridDim.x, ...
-// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA
-// issuer (whole warps, one elected lane issues), warps 2..9 two compute
-// warpgroups (thread = TMEM lane = stationary row).  Sub-chunk with global
-// index gu lives in TMEM buffer gu%2 and is processed by warpgroup gu%2, so
-// the tensor core computes the next sub-chunk while a warpgroup works:
-//   MMA order per tile: ST_0, ST_1, [P_0] OUT_0, ST_2, [P_1] OUT_1, ST_3, ...
-// Stationary tiles are double-buffered in smem and the output accumulators
-// in TMEM, so tile i+1's loads and MMAs overlap tile i's epilogue.
+// Warp roles (352 threads): warps 0..7 two compute warpgroups (thread = TMEM
+// lane = stationary row); warp 8 TMA producer (stationary tiles double-
+// buffered, 4-stage ring of streamed chunks + their row vectors); warp 9
+// TMEM owner + OUT-MMA issuer; warp 10 S/dP-MMA issuer (one elected lane
+// each).  Sub-chunk gu (64 partner columns) is processed by warpgroup gu%2:
+//   S/dP(gu) -> TMEM buffer gu%2; the warpgroup loads it (B_SF releases the
+//   buffer, so S/dP(gu+2) overlaps this softmax), computes P and dS, writes
+//   them packed to their own TMEM buffer gu%2 (B_P), and the OUT warp issues
+//   the accumulating MMAs in order (B_PE frees the packed buffer).
+// dK|dV share one 128-column accumulator drained at each tile start by the
+// warpgroup not owning the tile's first sub-chunk; dQ's is double-buffered.
+// Outputs are staged in the tile's dead stationary smem and TMA-stored.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>

@@ -3,11 +3,14 @@
 // One CTA handles 128-query multi-dimensional tiles, each of one residue
 // class of one (b, h) (§3.3 fused NA, Fig. 4; dilation as extra
 // tiles P:329-331).  Persistent: 2 CTAs per SM walk the tile list
-// blockIdx.x, blockIdx.x + gridDim.x, ...  Warp roles (192 threads):
-//   warp 0      TMA producer: Q box per tile (double-buffered), then K and V
+// blockIdx.x, blockIdx.x + gridDim.x, ...  Warp roles (192 threads; the
+// single-lane roles take the highest warp ids, which the scheduler favours):
+//   warps 0..3  softmax + epilogue: thread = query row = TMEM lane; the
+//               epilogue stages O in the tile's (dead) Q buffer and thread 0
+//               writes it with a TMA bulk-tensor store.
+//   warp 4      TMA producer: Q box per tile (double-buffered), then K and V
 //               boxes of every KV chunk of the tile's halo (2-stage ring).
-//   warp 1      TMEM owner + MMA issuer (whole warp, one elected lane).
-//   warps 2..5  softmax + epilogue: thread = query row = TMEM lane.
+//   warp 5      TMEM owner + MMA issuer (whole warp, one elected lane).
 // Each KV chunk (<= 128 keys, one TMA box) is consumed as <= 2 sub-chunks of
 // 64 keys whose S = Q K^T accumulators alternate between two TMEM buffers, so
 // the tensor core computes sub-chunk u+1 (and PV of u-1) while the softmax

@@ -62,8 +62,22 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifndef NA_MBAR_SUSPEND_NS
+#define NA_MBAR_SUSPEND_NS 0
+#endif
+// Blocking wait.  With NA_MBAR_SUSPEND_NS > 0 the waiting warp is suspended
+// (up to that many ns, woken when the phase completes) instead of spinning.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+#if NA_MBAR_SUSPEND_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity), "n"(NA_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -71,6 +85,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(a),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // ---------------------------------------------------------------------- TMA
