@@ -289,7 +289,7 @@ def oracle_sample(tokens: int, n_slices: int):
 def cpu_baseline_sample():
     import oracle
     cores = oracle.num_threads()
-    step, fl, desc = oracle_sample(4096, cores)
+    step, fl, desc = oracle_sample(6144, cores)
     t0 = time.perf_counter()
     step()
     dt = time.perf_counter() - t0
