@@ -426,15 +426,14 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       unsigned tile_n = num_tiles;
       bool tn_known = false;
       float nrow_nl2 = 0.f, nrow_d = 0.f;
-      uint32_t mw[4] = {0u, 0u, 0u, 0u};
       for (int u = u_first; u < nsub; u += 2) {
         if (issuer && u != u_first) release_store();  // the store has had a sub-chunk to read
         const uint32_t gu = ub + u;
         const int j = u / ns, h = u % ns;
         int org[3];
         t.chunk_origin(pl, j, org);
-        r.chunk_mask(pl, org, mw);
-        const uint32_t w[2] = {h ? mw[2] : mw[0], h ? mw[3] : mw[1]};
+        uint32_t w[2];
+        r.sub_mask(pl, org, h, w);
         // Partner (query) values of the chunk, TMA-loaded with it:
         // [-LSE*log2(e) x rows_kv | D x rows_kv]; this sub-chunk's 64 columns.
         const uint32_t kv = kv_base + j;
@@ -465,12 +464,10 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
 #pragma unroll
         for (int gq = 0; gq < 2; ++gq) {
           const bool any = __any_sync(0xffffffffu, w[gq] != 0u);
-          uint32_t sv[32], pv[32];
-          if (any) {
-            NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
-            NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
-            ptx::tmem_ld_wait();
-          }
+          uint32_t sv[32], pv[32];  // loaded unconditionally (a conditional load costs register zero-fills)
+          NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
+          NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
+          ptx::tmem_ld_wait();
           if (gq == 1) {
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar + B_SF + (gu & 1));

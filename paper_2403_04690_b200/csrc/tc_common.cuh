@@ -120,7 +120,7 @@ struct TileCtx {
         // instruction otherwise, tools/tma_probe.cu).  Extra columns are masked.
         if (a == RANK - 1) lo[a] &= ~3;
       }
-      nch[a] = (hi - lo[a] + pl.ckv[a]) / pl.ckv[a];
+      nch[a] = (int)fdiv((uint32_t)(hi - lo[a] + pl.ckv[a]), pl.f_ckv[a]);
       nchunks *= nch[a];
     }
 #pragma unroll
@@ -200,17 +200,19 @@ __device__ __forceinline__ unsigned seek_tile(const Geom& g, const TcPlan& pl, u
   return tile;
 }
 
-__device__ __forceinline__ void set_range(uint32_t mw[4], int lo, int hi) {
+// Bits [lo - 32*w0, hi - 32*w0] (inclusive, clipped) of 32-bit words w0, w0+1, ...
+// OR-ed into mw[0..NW); branch-free (64-bit shifts handle the 32-bit edge).
+template <int NW>
+__device__ __forceinline__ void set_range_w(uint32_t* mw, int lo, int hi, int w0) {
 #pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    int a = lo - 32 * w, b = hi - 32 * w;
-    if (b >= 0 && a <= 31 && a <= b) {
-      a = a < 0 ? 0 : a;
-      b = b > 31 ? 31 : b;
-      mw[w] |= (0xffffffffu >> (31 - (b - a))) << a;
-    }
+  for (int w = 0; w < NW; ++w) {
+    const int off = 32 * (w0 + w);
+    const int a = min(max(lo - off, 0), 32);
+    const int b = min(max(hi - off + 1, a), 32);
+    mw[w] |= (uint32_t)(((1ull << b) - 1ull) ^ ((1ull << a) - 1ull));
   }
 }
+__device__ __forceinline__ void set_range(uint32_t mw[4], int lo, int hi) { set_range_w<4>(mw, lo, hi, 0); }
 
 // One row (= one TMEM lane = one thread) of a stationary tile.
 template <int RANK>
@@ -254,6 +256,20 @@ struct RowCtx {
 
   // Validity bitmask of the <=128 chunk columns for this row: column
   // (lt*ckv1 + ly)*ckv2 + lx is the key at org + (lt, ly, lx).
+  // Validity bits of the 64 columns [64h, 64h + 64) of the chunk at `org`.
+  __device__ __forceinline__ void sub_mask(const TcPlan& pl, const int org[3], int h, uint32_t w[2]) const {
+    if constexpr (RANK == 1) {
+      w[0] = w[1] = 0u;
+      const int lo = max(wlo[0] - org[0], 0), hi = min(whi[0] - org[0], pl.ckv[0] - 1);
+      set_range_w<2>(w, lo, hi, 2 * h);
+    } else {
+      uint32_t mw[4];
+      chunk_mask(pl, org, mw);
+      w[0] = h ? mw[2] : mw[0];
+      w[1] = h ? mw[3] : mw[1];
+    }
+  }
+
   __device__ __forceinline__ void chunk_mask(const TcPlan& pl, const int org[3], uint32_t mw[4]) const {
     mw[0] = mw[1] = mw[2] = mw[3] = 0u;
     if constexpr (RANK == 1) {

@@ -141,6 +141,7 @@ TcPlan make_plan(const Geom& g, int tile_rows) {
     pl.tq_shift[a] = s;
     pl.f_dil[a] = make_fastdiv(a < g.rank ? g.dil[a] : 1);
     pl.f_ntile[a] = make_fastdiv(pl.ntile[a]);
+    pl.f_ckv[a] = make_fastdiv(pl.ckv[a]);
   }
   pl.f_tiles = make_fastdiv(pl.tiles);
   pl.f_nres = make_fastdiv(pl.nres);

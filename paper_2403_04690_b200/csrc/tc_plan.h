@@ -46,7 +46,7 @@ struct TcPlan {
   int kv_issues;   // TMA issues per K or V chunk
   int q_box_x;     // compacted x extent per Q issue
   int kv_box_x;    // compacted x extent per KV issue
-  FastDiv f_tiles, f_nres, f_dil[3], f_ntile[3];
+  FastDiv f_tiles, f_nres, f_dil[3], f_ntile[3], f_ckv[3];
 };
 
 }  // namespace na
