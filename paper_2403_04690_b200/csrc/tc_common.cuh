@@ -214,6 +214,16 @@ __device__ __forceinline__ void set_range_w(uint32_t* mw, int lo, int hi, int w0
 }
 __device__ __forceinline__ void set_range(uint32_t mw[4], int lo, int hi) { set_range_w<4>(mw, lo, hi, 0); }
 
+// 2^n - 1 for n in [0, 64] (n >= 64: all ones).
+__device__ __forceinline__ unsigned long long lowbits64(int n) {
+  return n >= 64 ? ~0ull : (n <= 0 ? 0ull : (1ull << n) - 1ull);
+}
+// OR bits [a, b] (a <= b, within [0, 128)) into the 128-bit value (lo, hi).
+__device__ __forceinline__ void range128(int a, int b, unsigned long long& lo, unsigned long long& hi) {
+  lo |= lowbits64(b + 1) & ~lowbits64(a);
+  hi |= lowbits64(b + 1 - 64) & ~lowbits64(a - 64);
+}
+
 // One row (= one TMEM lane = one thread) of a stationary tile.
 template <int RANK>
 struct RowCtx {
@@ -271,36 +281,48 @@ struct RowCtx {
   }
 
   __device__ __forceinline__ void chunk_mask(const TcPlan& pl, const int org[3], uint32_t mw[4]) const {
-    mw[0] = mw[1] = mw[2] = mw[3] = 0u;
     if constexpr (RANK == 1) {
+      mw[0] = mw[1] = mw[2] = mw[3] = 0u;
       int lo = wlo[0] - org[0], hi = whi[0] - org[0];
       lo = lo < 0 ? 0 : lo;
       hi = hi > pl.ckv[0] - 1 ? pl.ckv[0] - 1 : hi;
       set_range(mw, lo, hi);
     } else {
-      const int ax = RANK - 1;  // innermost axis
-      int xlo = wlo[ax] - org[ax], xhi = whi[ax] - org[ax];
-      xlo = xlo < 0 ? 0 : xlo;
-      xhi = xhi > pl.ckv[ax] - 1 ? pl.ckv[ax] - 1 : xhi;
-      if (xlo > xhi) return;
-      if constexpr (RANK == 2) {
-        for (int ly = 0; ly < pl.ckv[0]; ++ly) {
-          const int ky = org[0] + ly;
-          if (ky >= wlo[0] && ky <= whi[0]) set_range(mw, ly * pl.ckv[1] + xlo, ly * pl.ckv[1] + xhi);
-        }
-      } else {
-        for (int lt = 0; lt < pl.ckv[0]; ++lt) {
-          const int kt = org[0] + lt;
-          if (kt < wlo[0] || kt > whi[0]) continue;
-          for (int ly = 0; ly < pl.ckv[1]; ++ly) {
-            const int ky = org[1] + ly;
-            if (ky >= wlo[1] && ky <= whi[1]) {
-              const int base = (lt * pl.ckv[1] + ly) * pl.ckv[2];
-              set_range(mw, base + xlo, base + xhi);
-            }
+      // window on the innermost axis, replicated on every chunk row by one
+      // multiplication, then AND-ed with the rows whose outer coordinates are
+      // inside the window (an interval of rows per outermost index).
+      constexpr int ax = RANK - 1;
+      const int cx = pl.ckv[ax];
+      const int xlo = max(wlo[ax] - org[ax], 0), xhi = min(whi[ax] - org[ax], cx - 1);
+      const int ylo = max(wlo[ax - 1] - org[ax - 1], 0), yhi = min(whi[ax - 1] - org[ax - 1], pl.ckv[ax - 1] - 1);
+      unsigned long long rlo = 0ull, rhi = 0ull;
+      if (cx > 64) {  // then the chunk is a single row of the innermost axis
+        bool ok = xlo <= xhi && ylo <= yhi;
+        if constexpr (RANK == 3) ok = ok && wlo[0] <= org[0] && org[0] <= whi[0];
+        if (ok) range128(xlo, xhi, rlo, rhi);
+      } else if (xlo <= xhi && ylo <= yhi) {
+        const unsigned long long xm = lowbits64(xhi + 1) & ~lowbits64(xlo);  // cx <= 64 when rows > 1
+        const unsigned long long rep_lo = xm * pl.rep_lo;
+        const unsigned long long rep_hi = xm * pl.rep_hi | (pl.rep_sh ? xm >> pl.rep_sh : 0ull);
+        if constexpr (RANK == 2) {
+          range128(ylo * cx, (yhi + 1) * cx - 1, rlo, rhi);
+        } else {
+          const int c1 = pl.ckv[1];
+          const int tlo = max(wlo[0] - org[0], 0), thi = min(whi[0] - org[0], pl.ckv[0] - 1);
+          if (ylo == 0 && yhi == c1 - 1) {  // whole y extent: one interval of rows
+            if (tlo <= thi) range128(tlo * c1 * cx, (thi + 1) * c1 * cx - 1, rlo, rhi);
+          } else {
+            for (int lt = tlo; lt <= thi; ++lt)
+              range128((lt * c1 + ylo) * cx, (lt * c1 + yhi + 1) * cx - 1, rlo, rhi);
           }
         }
+        rlo &= rep_lo;
+        rhi &= rep_hi;
       }
+      mw[0] = (uint32_t)rlo;
+      mw[1] = (uint32_t)(rlo >> 32);
+      mw[2] = (uint32_t)rhi;
+      mw[3] = (uint32_t)(rhi >> 32);
     }
   }
 };

@@ -143,6 +143,18 @@ TcPlan make_plan(const Geom& g, int tile_rows) {
     pl.f_ntile[a] = make_fastdiv(pl.ntile[a]);
     pl.f_ckv[a] = make_fastdiv(pl.ckv[a]);
   }
+  {
+    const int cx = pl.ckv[g.rank - 1];
+    const int rows = pl.rows_kv / cx;
+    pl.rep_lo = pl.rep_hi = 0ull;
+    pl.rep_sh = 0;
+    for (int i = 0; i < rows; ++i) {
+      const int b = i * cx;
+      if (b < 64) pl.rep_lo |= 1ull << b;
+      else if (b < 128) pl.rep_hi |= 1ull << (b - 64);
+      if (b < 64 && b + cx > 64) pl.rep_sh = 64 - b;
+    }
+  }
   pl.f_tiles = make_fastdiv(pl.tiles);
   pl.f_nres = make_fastdiv(pl.nres);
   return pl;

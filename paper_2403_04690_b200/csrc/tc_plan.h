@@ -47,6 +47,14 @@ struct TcPlan {
   int q_box_x;     // compacted x extent per Q issue
   int kv_box_x;    // compacted x extent per KV issue
   FastDiv f_tiles, f_nres, f_dil[3], f_ntile[3], f_ckv[3];
+  // Multi-dimensional chunk masks (RowCtx::chunk_mask): a chunk column is
+  // (row, lx) with row = the chunk's outer coordinates flattened and lx the
+  // innermost one, at bit row * cx + lx.  rep = sum over rows of 2^(row*cx)
+  // as two 64-bit halves; rep_sh = 64 - row* * cx for the row straddling
+  // bit 64 (0: none).  x-window bits times rep = the window replicated on
+  // every row (the copies never overlap, so the product has no carries).
+  unsigned long long rep_lo, rep_hi;
+  int rep_sh;
 };
 
 }  // namespace na
