@@ -96,7 +96,6 @@ enum : int {
 // chunks b0, b1; output tiles out0 (, out1) stored with TMA (stationary box).
 struct BwdMaps {
   CUtensorMap a0, a1, b0, b1, out0, out1;
-  CUtensorMap rv;  // dK/dV: the streamed chunk's row vector (-LSE*log2(e), D)
 };
 
 template <int RANK, int D, bool BF16, bool KV_STATIONARY>
@@ -134,7 +133,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       ptx::mbar_init(bar + B_OE + b, KV_STATIONARY ? 128 : kCompute);
     }
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(bar + B_B + s, 1);
+      // dK/dV: + one cp.async arrival per producer lane (row-vector gather)
+      ptx::mbar_init(bar + B_B + s, KV_STATIONARY ? 33 : 1);
       ptx::mbar_init(bar + B_E + s, 1);
     }
     ptx::fence_barrier_init();
@@ -162,7 +162,11 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     ptx::tma_prefetch(&map_a1);
     ptx::tma_prefetch(&map_b0);
     ptx::tma_prefetch(&map_b1);
-    const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes + (KV_STATIONARY ? 2 * pl.rows_kv * 4 : 0);
+    const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes;
+    // dK/dV: the streamed chunk's row vectors (-LSE*log2(e), D) are gathered
+    // with 4-byte cp.async by the 32 producer lanes (columns lane, lane+32,
+    // ...): chunk origins need no 16-byte alignment, unlike a TMA box.
+    const FastDiv f_cx = pl.f_ckv[RANK - 1], f_cy = pl.f_ckv[RANK >= 2 ? RANK - 2 : 0];
     uint32_t kv_it = 0, ti = 0;
     int tr = 0;
     (void)tr;
@@ -194,7 +198,41 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           t.template load_box<RANK>(&map_b1, smem + S::kB1 + s * S::kTile + i * pl.kv_box_x * S::kRowBytes,
                                     bar + B_B + s, org, i * pl.kv_box_x, g);
         }
-        if constexpr (KV_STATIONARY) t.template load_rv<RANK>(&maps.rv, vec + s * 256, bar + B_B + s, org, g);
+        if constexpr (KV_STATIONARY) {
+          const float* src = rv + rv_base(g, t.bh, t.res);
+          float* dst = vec + s * 256;
+          for (int c = lane; c < pl.rows_kv; c += 32) {
+            int l[3] = {0, 0, 0};
+            if constexpr (RANK == 1) {
+              l[0] = c;
+            } else {
+              const uint32_t rest = fdiv((uint32_t)c, f_cx);
+              l[RANK - 1] = c - (int)(rest * f_cx.d);
+              if constexpr (RANK == 2) {
+                l[0] = (int)rest;
+              } else {
+                const uint32_t r2 = fdiv(rest, f_cy);
+                l[1] = (int)(rest - r2 * f_cy.d);
+                l[0] = (int)r2;
+              }
+            }
+            bool in = true;
+            long long off = 0;
+#pragma unroll
+            for (int a = 0; a < RANK; ++a) {
+              const int x = org[a] + l[a];
+              in = in && x < g.rv_lc[a];
+              off += (long long)x * g.rv_cs[a];
+            }
+            // columns outside the padded class extents keep finite stale
+            // values; they are masked (P = 0) by every row
+            if (in) {
+              ptx::cp_async4(dst + c, src + off);
+              ptx::cp_async4(dst + 128 + c, src + g.rv_plane + off);
+            }
+          }
+          ptx::cp_async_mbar_arrive_noinc(bar + B_B + s);
+        }
       }
       ++ti;
     }
@@ -435,10 +473,10 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         uint32_t w[2];
         r.sub_mask(pl, org, h, w);
         // Partner (query) values of the chunk, TMA-loaded with it:
-        // [-LSE*log2(e) x rows_kv | D x rows_kv]; this sub-chunk's 64 columns.
+        // [-LSE*log2(e) x 128 | D x 128] (cp.async-gathered); this sub-chunk's 64 columns.
         const uint32_t kv = kv_base + j;
         const float* cl = vec + (kv % kStages) * 256 + h * 64;
-        const float* cd = cl + pl.rows_kv;
+        const float* cd = cl + 128;
         if (u + 2 >= nsub) {
           tile_n = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, tn);
           tn_known = true;
@@ -662,8 +700,6 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   if ((e = make_map(&mkv.out1, dtype, g, dv, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
   if ((e = make_map(&mq.out0, dtype, g, dq, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
   mq.out1 = mq.out0;
-  if ((e = make_map_rv(&mkv.rv, g, Dvec, pl.ckv)) != cudaSuccess) return e;
-  mq.rv = mkv.rv;
   *launches = 3;
   switch (g.rank) {
     case 1: return by_type<1>(dtype, g, pl, mkv, mq, Dvec, st);

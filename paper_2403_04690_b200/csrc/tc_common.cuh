@@ -18,9 +18,6 @@ TcPlan make_plan(const Geom& g, int tile_rows);
 int num_sms();  // SMs of the current device (cached per device)
 cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base,
                      const int box[3], int box_x);
-// fp32 map over the backward row-vector layout (Geom::rv_*): dims (innermost
-// first) X'_{R-1}, ..., X'_0, plane, BH*nres; box = one chunk x both planes.
-cudaError_t make_map_rv(CUtensorMap* map, const Geom& g, const float* base, const int box[3]);
 
 template <bool BF16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -115,10 +112,6 @@ struct TileCtx {
       } else {
         lo[a] = inv_start(q_origin[a], Lr[a], g.k[a], g.causal[a]);
         hi = inv_end(q_origin[a] + qv[a] - 1, Lr[a], g.k[a], g.causal[a]);
-        // Innermost chunk origins on a multiple of 4: the fp32 row-vector TMA
-        // box must start 16-byte aligned (measured: sm_100a raises an illegal
-        // instruction otherwise, tools/tma_probe.cu).  Extra columns are masked.
-        if (a == RANK - 1) lo[a] &= ~3;
       }
       nch[a] = (int)fdiv((uint32_t)(hi - lo[a] + pl.ckv[a]), pl.f_ckv[a]);
       nchunks *= nch[a];
@@ -157,20 +150,6 @@ struct TileCtx {
     } else {
       ptx::tma_load_5d_w(dst, m, bar, 0, r[2] + g.dil[2] * (org[2] + x_off),
                        r[1] + g.dil[1] * org[1], r[0] + g.dil[0] * org[0], bh);
-    }
-  }
-
-  // TMA load of the row-vector box (both planes) of the chunk at `org`.
-  template <int R>
-  __device__ __forceinline__ void load_rv(const CUtensorMap* m, void* dst, uint64_t* bar, const int org[3],
-                                          const Geom& g) const {
-    const int bhres = bh * g.nres + res;
-    if constexpr (R == 1) {
-      ptx::tma_load_3d_w(dst, m, bar, org[0], 0, bhres);
-    } else if constexpr (R == 2) {
-      ptx::tma_load_4d_w(dst, m, bar, org[1], org[0], 0, bhres);
-    } else {
-      ptx::tma_load_5d_w(dst, m, bar, org[2], org[1], org[0], 0, bhres);
     }
   }
 

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <climits>
 #include <mutex>
+#include <vector>
 
 #include "na_geom.cuh"
 #include "na_kernels.h"
@@ -44,7 +45,9 @@ int box_x_for(int ext, int dil) {
 
 }  // namespace
 
-TcPlan make_plan(const Geom& g, int tile_rows) {
+namespace {
+
+TcPlan make_plan_uncached(const Geom& g, int tile_rows) {
   TcPlan pl{};
   int Lmax[3];
   for (int a = 0; a < 3; ++a) {
@@ -59,54 +62,51 @@ TcPlan make_plan(const Geom& g, int tile_rows) {
     pl.q_box_x = box_x_for(tile_rows, g.dil[0]);
     pl.kv_box_x = box_x_for(128, g.dil[0]);
   } else {
-    // Enumerate power-of-two tiles (product tile_rows) and KV boxes covering the
-    // interior halo t + k - 1; minimise MMA columns (+ per-chunk overhead) per
-    // useful query row.
+    // Enumerate power-of-two query tiles (product tile_rows) and every KV
+    // chunk box that tiles the tile's interior halo t + k - 1 per axis with
+    // balanced extents (ceil(h / n) for n chunks); minimise the cost of the
+    // softmax rounds per useful query row: chunks * (MMA columns + a fixed
+    // per-round cost of kRoundCols columns).
+    constexpr int kRoundCols = 96;
     const int R = g.rank;
     double best = 1e30;
-    int t[3] = {1, 1, 1};
     auto consider = [&](const int tq[3]) {
-      int h[3], valid_rows = 1;
+      int h[3] = {1, 1, 1}, valid_rows = 1;
       for (int a = 0; a < R; ++a) {
         if (tq[a] * g.dil[a] > 256) return;
         h[a] = std::min(tq[a] + g.k[a] - 1, Lmax[a]);
         valid_rows *= std::min(tq[a], Lmax[a]);
       }
-      const int ax = R - 1;
-      // candidate innermost box widths
-      for (int split = 1; split <= 4; ++split) {
-        // multiple of 4: the fp32 row-vector box's inner extent must be 16 bytes
-        int cx = (ceil_div(h[ax], split) + 3) / 4 * 4;
-        if (cx > 128 || cx * g.dil[ax] > 256) continue;
-        int ck[3] = {1, 1, 1};
-        ck[ax] = cx;
-        int room = 128 / cx;
-        // fill remaining axes from inner to outer, balancing chunk counts
-        for (int a = ax - 1; a >= 0; --a) {
-          int c = std::min(h[a], room);
-          if (c < 1) c = 1;
-          int n = ceil_div(h[a], c);
-          c = ceil_div(h[a], n);  // balance
-          while (c * g.dil[a] > 256) c--;
-          ck[a] = c;
-          room = std::max(1, room / c);
-        }
-        int rows = 1, chunks = 1;
-        for (int a = 0; a < R; ++a) {
-          rows *= ck[a];
-          chunks *= ceil_div(h[a], ck[a]);
-        }
-        if (rows > 128) continue;
-        const double cost = (double)chunks * (round16(rows) + 48) / valid_rows;
-        if (cost < best) {
-          best = cost;
-          for (int a = 0; a < 3; ++a) {
-            pl.tq[a] = a < R ? tq[a] : 1;
-            pl.ckv[a] = a < R ? ck[a] : 1;
-          }
+      int opts[3][160], nopt[3] = {1, 1, 1};
+      for (int a = 0; a < 3; ++a) opts[a][0] = 1;
+      for (int a = 0; a < R; ++a) {
+        nopt[a] = 0;
+        int last = -1;
+        for (int n = 1; n <= h[a] && nopt[a] < 160; ++n) {
+          const int c = ceil_div(h[a], n);
+          if (c == last || c > 128 || c * g.dil[a] > 256) continue;
+          opts[a][nopt[a]++] = last = c;
         }
       }
+      for (int i0 = 0; i0 < nopt[0]; ++i0)
+        for (int i1 = 0; i1 < nopt[1]; ++i1)
+          for (int i2 = 0; i2 < nopt[2]; ++i2) {
+            const int ck[3] = {opts[0][i0], opts[1][i1], opts[2][i2]};
+            const int rows = ck[0] * ck[1] * ck[2];
+            if (rows > 128) continue;
+            int chunks = 1;
+            for (int a = 0; a < R; ++a) chunks *= ceil_div(h[a], ck[a]);
+            const double cost = (double)chunks * (round16(rows) + kRoundCols) / valid_rows;
+            if (cost < best) {
+              best = cost;
+              for (int a = 0; a < 3; ++a) {
+                pl.tq[a] = a < R ? tq[a] : 1;
+                pl.ckv[a] = a < R ? ck[a] : 1;
+              }
+            }
+          }
     };
+    int t[3] = {1, 1, 1};
     if (R == 2) {
       for (int tx = 1; tx <= tile_rows; tx *= 2) {
         t[1] = tx;
@@ -157,6 +157,39 @@ TcPlan make_plan(const Geom& g, int tile_rows) {
   }
   pl.f_tiles = make_fastdiv(pl.tiles);
   pl.f_nres = make_fastdiv(pl.nres);
+  return pl;
+}
+
+}  // namespace
+
+// Plans depend only on the geometry; the multi-dimensional search costs
+// ~1 ms, so plans are cached per process (small linear table, mutex).
+TcPlan make_plan(const Geom& g, int tile_rows) {
+  struct Entry {
+    int key[14];
+    TcPlan plan;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int key[14] = {g.rank, tile_rows};
+  for (int a = 0; a < 3; ++a) {
+    key[2 + a] = g.L[a];
+    key[5 + a] = g.k[a];
+    key[8 + a] = g.dil[a];
+    key[11 + a] = g.causal[a];
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry& e : cache)
+      if (std::equal(key, key + 14, e.key)) return e.plan;
+  }
+  const TcPlan pl = make_plan_uncached(g, tile_rows);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 256) cache.erase(cache.begin());
+  Entry e;
+  std::copy(key, key + 14, e.key);
+  e.plan = pl;
+  cache.push_back(e);
   return pl;
 }
 
@@ -227,33 +260,6 @@ cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* bas
                    R + 2, const_cast<void*>(base), dims, strides, boxd, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
-cudaError_t make_map_rv(CUtensorMap* map, const Geom& g, const float* base, const int box[3]) {
-  EncodeTiled enc = encoder();
-  if (!enc) return cudaErrorNotSupported;
-  const int R = g.rank;
-  cuuint64_t dims[5], strides[4];
-  cuuint32_t boxd[5], estr[5];
-  for (int i = 0; i < R; ++i) {  // i = 0 innermost
-    const int a = R - 1 - i;
-    dims[i] = g.rv_lc[a];
-    if (i > 0) strides[i - 1] = (cuuint64_t)g.rv_cs[a] * 4;
-    boxd[i] = (cuuint32_t)box[a];
-    estr[i] = 1;
-  }
-  dims[R] = 2;  // planes: -LSE*log2(e), D
-  strides[R - 1] = (cuuint64_t)g.rv_plane * 4;
-  boxd[R] = 2;
-  estr[R] = 1;
-  dims[R + 1] = (cuuint64_t)g.BH * g.nres;
-  strides[R] = (cuuint64_t)g.rv_plane * 8;
-  boxd[R + 1] = 1;
-  estr[R + 1] = 1;
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, R + 2, const_cast<float*>(base), dims, strides, boxd,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
