@@ -16,6 +16,10 @@ l = 255.  Multi-GPU (torchrun): each rank owns its own contiguous range of
 B*H slices (weak scaling, no collective on the data path); NCCL only gathers
 timings.  Device time = CUDA events on the launch stream, max over ranks.
 
+`per_config` in the JSON line: fwd ms and fwd+bwd ms of EVERY BASELINE.json
+config (B's four variants, C at dilation 1 and 8, D, E), with effective
+TFLOP/s and the fractions of the tensor peak and (forward) of HBM bandwidth.
+
 `--impl reference`: the arm the driver compares against is the fp64 CPU
 oracle (oracle/, test infrastructure) timed on this host's cores on a
 bounded sample of the same workload (tier rules).
@@ -297,6 +301,65 @@ def cpu_baseline_sample():
             "sample": desc + f"; {dt:.1f} s", "seconds": round(dt, 2)}
 
 
+PER_CONFIG = ["B_d1", "B_d1_causal", "B_d4", "B_d4_causal", "C_d1", "C_d8", "D_d2", "E"]
+
+
+def per_config_table(args, world, rank, peaks):
+    """Every BASELINE.json config: fwd ms and fwd+bwd ms
+    (CUDA events, L2 flushed before each call, max over ranks), effective
+    TFLOP/s with the paper's nominal FLOPs, and the fractions of the B200
+    tensor peak and (forward) of HBM bandwidth.  Weak scaling: each rank owns
+    its own B*H slices of the config (seeded by global slice index)."""
+    import paper_2403_04690_b200 as na
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    peak_tf = float(peaks.get("bf16_tflops", 1590.0))
+    peak_bw = float(peaks["hbm_gbs"])
+    out = {}
+    n = max(3, min(args.steps, 10))
+    for name in PER_CONFIG:
+        cfg = na_synth.CONFIGS[name]
+        bh = cfg.batch * cfg.heads
+        q, k, v, do = na_synth.make_inputs(cfg, device="cuda", bh_range=shard_range(rank, bh))
+        shape = cfg.shape()
+        q, k, v, do = (t.view(shape) for t in (q, k, v, do))
+        kw = dict(kernel_size=list(cfg.kernel_size), dilation=list(cfg.dilation),
+                  is_causal=[bool(c) for c in cfg.is_causal])
+        o = torch.empty_like(q)
+        lse = torch.empty(shape[:-1], dtype=torch.float32, device="cuda")
+        dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+        pr = na.make_problem(cfg.batch, cfg.heads, list(cfg.extent), cfg.head_dim, **kw, dtype=cfg.dtype)
+        ws = torch.empty((na.na_bwd_workspace_size(pr) + 3) // 4, dtype=torch.float32, device="cuda")
+
+        def fwd():
+            na.na_fwd(q, k, v, out=o, lse=lse, **kw)
+
+        def fwd_bwd():
+            fwd()
+            na.na_bwd(q, k, v, o, do, lse, dq=dq, dk=dk, dv=dv, workspace=ws, **kw)
+
+        for _ in range(2):
+            fwd_bwd()
+        torch.cuda.synchronize()
+        barrier(world)
+        f_ms = reduce_max(statistics.median(timed_steps(fwd, n, flush)), world)
+        fb_ms = reduce_max(statistics.median(timed_steps(fwd_bwd, n, flush)), world)
+        fl_f = world * flops(cfg, fwd=True, bwd=False)
+        fl_fb = world * flops(cfg)
+        E = cfg.batch * cfg.heads * cfg.tokens * cfg.head_dim
+        fwd_bytes = world * (4 * E * 2 + 4 * cfg.batch * cfg.heads * cfg.tokens)
+        out[name] = {
+            "fwd_ms": round(f_ms, 4), "fwd_bwd_ms": round(fb_ms, 4),
+            "fwd_tflops": round(fl_f / (f_ms * 1e-3) / 1e12, 2),
+            "fwd_bwd_tflops": round(fl_fb / (fb_ms * 1e-3) / 1e12, 2),
+            "fwd_tensor_peak_frac": round(fl_f / (f_ms * 1e-3) / 1e12 / (world * peak_tf), 4),
+            "fwd_bwd_tensor_peak_frac": round(fl_fb / (fb_ms * 1e-3) / 1e12 / (world * peak_tf), 4),
+            "fwd_hbm_frac": round(fwd_bytes / (f_ms * 1e-3) / 1e9 / (world * peak_bw), 4),
+        }
+        del q, k, v, do, o, lse, dq, dk, dv, ws
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_native(args, world, rank, local):
     na_peaks, peak_src = load_peaks()
     R = Runner(rank)
@@ -379,6 +442,10 @@ def run_native(args, world, rank, local):
         e2e = {"value": world * step_flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
+    per_config = None
+    if not args.no_per_config:
+        per_config = per_config_table(args, world, rank, na_peaks)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -405,6 +472,7 @@ def run_native(args, world, rank, local):
                      "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
                      "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src,
                      "step_share": shares},
+        "per_config": per_config,
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
@@ -448,6 +516,8 @@ def main():
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true",
+                    help="skip the fwd / fwd+bwd table of every BASELINE.json config")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
