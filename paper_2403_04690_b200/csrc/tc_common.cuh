@@ -136,6 +136,17 @@ struct TileCtx {
     }
   }
 
+  // Odometer step from chunk j's origin to chunk j+1's (innermost axis
+  // fastest, the order of chunk_origin) without divisions.
+  __device__ __forceinline__ void next_origin(const TcPlan& pl, int org[3]) const {
+#pragma unroll
+    for (int a = RANK - 1; a >= 0; --a) {
+      org[a] += pl.ckv[a];
+      if (a == 0 || org[a] < lo[a] + nch[a] * pl.ckv[a]) break;
+      org[a] = lo[a];
+    }
+  }
+
   // TMA load of a box whose compacted corner is `org` (+x_off on the
   // innermost axis).  Coordinates are original-tensor element coordinates
   // r + dil * c; the tensor map's elementStrides = dil walks the class.

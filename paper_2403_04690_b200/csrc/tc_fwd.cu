@@ -16,15 +16,16 @@
 //               after its PV MMA).
 //   warp 7      TMEM owner + MMA issuer (whole warp, one elected lane).
 // Each KV chunk (<= 128 keys, one TMA box) is one softmax round: one
-// S = Q K^T MMA of N = n_kv (<= 128) columns into a single TMEM S buffer,
-// the softmax writes P over it as 16-bit, then O += P V.  The MMA order
-//   S_0, [P_0] PV_0, S_1, [P_1] PV_1, ...   (S_{j+1} follows PV_j in issue
-// order, so it may reuse the buffer PV_j reads)
-// keeps one CTA's tensor work to the gap between its softmax rounds; the
-// second CTA on the SM fills that gap (ping-pong).  S_{j} completing implies
-// PV_{j-1} is done, so O is stable while the softmax rescales it.  O is
-// double-buffered in TMEM so the epilogue of tile i overlaps the first MMAs
-// of tile i+1.
+// S = Q K^T MMA of N = n_kv (<= 128) columns into the TMEM S buffer; the
+// softmax warps load it and release the buffer at once (B_SF), so the next
+// round's S MMA runs under this round's exponentials; P goes to its own TMEM
+// buffer, then O += P V.  MMA issue order:
+//   S_0, [SF_0] S_1, [P_0] PV_0, [SF_1] S_2, [P_1] PV_1, ...
+// The softmax warps wait for PV_{kv-1} (B_PF) only before overwriting P or
+// rescaling O, i.e. never in steady state: they run back to back, the
+// tensor core fills the gaps, and the second CTA on the SM shares the pipes.
+// O is single-buffered: the next tile's PV_0 needs that tile's P_0, which the
+// softmax warps write only after their epilogue has read O.
 // Softmax per round (the whole round's logits of a row in registers):
 // tcgen05.ld the row's logits, neighborhood mask (per-row window bitmask)
 // applied only to 32-column groups that are partially valid for the warp,
@@ -58,9 +59,12 @@ constexpr int kMmaWarp = 7;
 // gives its share to the softmax warpgroup, which holds a whole 128-column
 // round of logits in registers.  128 * (kRegsSoftmax + kRegsOther) = the
 // 2-CTA/SM budget of 256 threads x 128.
-constexpr uint32_t kRegsSoftmax = 192;
-constexpr uint32_t kRegsOther = 64;
-constexpr uint32_t kColO = 128;  // O accumulators: [128, 128+D) and [128+D, 128+2D)
+constexpr uint32_t kRegsSoftmax = 200;
+constexpr uint32_t kRegsOther = 56;
+// TMEM columns (256 per CTA, two CTAs per SM): S [0, 128) fp32 logits of the
+// current round; P [128, 192) the previous round's probabilities as packed
+// 16-bit pairs (A operand of PV); O [192, 192 + D) the fp32 accumulator.
+constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 
 template <int D>
 struct FwdSmem {
@@ -81,11 +85,12 @@ enum : int {
   B_V = B_K + kStages,      // V stage full [kStages]
   B_KE = B_V + kStages,     // K stage free (its S MMA is done) [kStages]
   B_VE = B_KE + kStages,    // V stage free (its PV MMA is done) [kStages]
-  B_S = B_VE + kStages,     // S of the current round ready
-  B_P = B_S + 1,            // P of the current round written (128 arrivals)
-  B_OF = B_P + 1,           // O buffer full [2]
-  B_OE = B_OF + 2,          // O buffer drained by the epilogue [2] (128 arrivals)
-  B_COUNT = B_OE + 2
+  B_S = B_VE + kStages,     // S of a round ready
+  B_SF = B_S + 1,           // S loaded by the softmax warps: buffer free (128 arrivals)
+  B_P = B_SF + 1,           // P of a round written (128 arrivals)
+  B_PF = B_P + 1,           // PV of a round done: P buffer free, O stable
+  B_OF = B_PF + 1,          // O of a tile final
+  B_COUNT = B_OF + 1
 };
 
 // Tensor maps: Q tiles, K and V chunks, and O tiles (TMA store, Q's box).
@@ -115,9 +120,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(bar + B_QF + b, 1);
       ptx::mbar_init(bar + B_QE + b, 1);
-      ptx::mbar_init(bar + B_OF + b, 1);
-      ptx::mbar_init(bar + B_OE + b, kSoftmax);
     }
+    ptx::mbar_init(bar + B_OF, 1);
+    ptx::mbar_init(bar + B_SF, kSoftmax);
+    ptx::mbar_init(bar + B_PF, 1);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(bar + B_K + s, 1);
       ptx::mbar_init(bar + B_V + s, 1);
@@ -164,11 +170,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int i = 0; i < pl.q_issues; ++i)
         t.template load_box<RANK>(&map_q, smem + S::kQ + qb * S::kTile + i * pl.q_box_x * S::kRowBytes,
                                   bar + B_QF + qb, t.q_origin, i * pl.q_box_x, g);
-      for (int j = 0; j < t.nchunks; ++j, ++kv_it) {
+      int org[3] = {t.lo[0], t.lo[1], t.lo[2]};
+      for (int j = 0; j < t.nchunks; ++j, ++kv_it, t.next_origin(pl, org)) {
         const int s = kv_it % kStages;
         const uint32_t ph = ((kv_it / kStages) - 1) & 1;
-        int org[3];
-        t.chunk_origin(pl, j, org);
         uint8_t* kd = smem + S::kK + s * S::kTile;
         uint8_t* vd = smem + S::kV + s * S::kTile;
         if (kv_it >= kStages) ptx::mbar_wait(bar + B_KE + s, ph);
@@ -186,14 +191,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       ++ti;
     }
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (whole warp, one lane issues) =====================
+    // ===================== MMA issuer (whole warp, one elected lane) =====================
+    // Issue order S_0, [SF_0] S_1, [P_0] PV_0, [SF_1] S_2, [P_1] PV_1, ...:
+    // S_{kv+1} starts as soon as the softmax warps have LOADED S_kv, so it
+    // overlaps their exponentials; PV_kv reads P from its own buffer.
     constexpr uint32_t kSw = D == 64 ? 2u : 4u;  // SW128 : SW64
     constexpr uint32_t kSbo = 8 * S::kRowBytes;  // 8-row core-matrix group
     const uint32_t idesc_s = ptx::make_idesc(128, pl.n_kv, BF16, false);
     constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
     const int kblocks = pl.n_kv / 16;
-    // S = Q K_kv^T (K-dim = head_dim) into the S buffer; kv = global chunk index
     int tr = 0;
+    // S = Q K_kv^T (K-dim = head_dim); kv = global chunk index
     auto issue_s = [&](uint32_t kv, uint32_t q_addr) {
       const int s = kv % kStages;
       ptx::mbar_wait(bar + B_K + s, (kv / kStages) & 1);
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t k_addr = ptx::smem_u32(smem + S::kK + s * S::kTile);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
-        ptx::mma_ss_w(tmem, ptx::make_sdesc(q_addr + kk * 32, 16, kSbo, kSw),
+        ptx::mma_ss_w(tmem + kColS, ptx::make_sdesc(q_addr + kk * 32, 16, kSbo, kSw),
                       ptx::make_sdesc(k_addr + kk * 32, 16, kSbo, kSw), idesc_s, kk > 0);
       ptx::mma_commit_w(bar + B_S);
       ptx::mma_commit_w(bar + B_KE + s);
@@ -216,33 +224,39 @@ __global__ void __launch_bounds__(kThreads, 2)
       issue_s(0, q_addr_of(0));
     }
     while (tile < num_tiles) {
-      const int ob = ti & 1;
-      const uint32_t o_col = kColO + ob * D;
       const int nch = t.nchunks;
+      TileCtx<RANK> tn;
+      unsigned tile_n = num_tiles;
       for (int j = 0; j < nch; ++j, ++kv) {
         const int s = kv % kStages;
-        ptx::mbar_wait(bar + B_P, kv & 1);  // softmax wrote P_j (and rescaled O)
+        // next S as soon as the softmax warps have read this one
+        ptx::mbar_wait(bar + B_SF, kv & 1);
+        if (j + 1 < nch) {
+          issue_s(kv + 1, q_addr_of(ti));
+        } else {
+          tile_n = seek_tile<RANK, false>(g, pl, tile + gridDim.x, num_tiles, tn);
+          if (tile_n < num_tiles) {  // first S of the next tile
+            ptx::mbar_wait(bar + B_QF + ((ti + 1) & 1), ((ti + 1) >> 1) & 1);
+            issue_s(kv + 1, q_addr_of(ti + 1));
+          }
+        }
+        ptx::mbar_wait(bar + B_P, kv & 1);  // softmax wrote P_kv (and rescaled O)
         NA_TRACE_EV(1, tr, 11);
-        // O buffer ob must have been drained by the epilogue of tile ti - 2
-        if (j == 0 && ti >= 2) ptx::mbar_wait(bar + B_OE + ob, ((ti >> 1) - 1) & 1);
         ptx::mbar_wait(bar + B_V + s, (kv / kStages) & 1);
         ptx::tc_fence_after();
         const uint32_t v_addr = ptx::smem_u32(smem + S::kV + s * S::kTile);
         for (int kk = 0; kk < kblocks; ++kk)  // O += P V, K-dim = keys
-          ptx::mma_ts_w(tmem + o_col, tmem + kk * 8,
+          ptx::mma_ts_w(tmem + kColO, tmem + kColP + kk * 8,
                         ptx::make_sdesc(v_addr + kk * 16 * S::kRowBytes, 128 * S::kRowBytes, kSbo, kSw),
                         idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         ptx::mma_commit_w(bar + B_VE + s);  // V stage free after these MMAs
+        ptx::mma_commit_w(bar + B_PF);      // P buffer free, O stable
+        if (j == nch - 1) ptx::mma_commit_w(bar + B_OF);
         NA_TRACE_EV(1, tr, 12);
-        if (j == nch - 1) ptx::mma_commit_w(bar + B_OF + ob);
-        else issue_s(kv + 1, q_addr_of(ti));
       }
-      tile = seek_tile<RANK, false>(g, pl, tile + gridDim.x, num_tiles, t);
+      tile = tile_n;
+      t = tn;
       ++ti;
-      if (tile < num_tiles) {  // first S of the next tile overlaps this tile's epilogue
-        ptx::mbar_wait(bar + B_QF + (ti & 1), (ti >> 1) & 1);
-        issue_s(kv, q_addr_of(ti));
-      }
     }
   }
   } else {
@@ -259,18 +273,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       TileCtx<RANK> t;
       if (!t.init(g, pl, tile)) continue;
-      const int ob = ti & 1;
-      const uint32_t o_col = kColO + ob * D;
       RowCtx<RANK> r;
       r.init(g, pl, t, row);
       float m_ref = -INFINITY, l = 0.f;
+      int org[3] = {t.lo[0], t.lo[1], t.lo[2]};  // chunk origin (odometer)
+      uint32_t mw[4];                             // this row's mask of the chunk
+      r.chunk_mask(pl, org, mw);
       for (int j = 0; j < t.nchunks; ++j, ++kv) {
-        uint32_t mw[4];
-        {
-          int org[3];
-          t.chunk_origin(pl, j, org);
-          r.chunk_mask(pl, org, mw);
-        }
         bool live[4];
 #pragma unroll
         for (int gq = 0; gq < 4; ++gq) live[gq] = __any_sync(0xffffffffu, mw[gq] != 0u);
@@ -282,8 +291,16 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint32_t sv[128];
 #pragma unroll
         for (int gq = 0; gq < 4; ++gq)
-          if (live[gq]) NA_TMEM_LD32(trow + 32 * gq, (sv + 32 * gq));
+          if (live[gq]) NA_TMEM_LD32(trow + kColS + 32 * gq, (sv + 32 * gq));
+        // the next chunk's mask, in the shadow of the TMEM load latency
+        uint32_t mwn[4] = {0u, 0u, 0u, 0u};
+        if (j + 1 < t.nchunks) {
+          t.next_origin(pl, org);
+          r.chunk_mask(pl, org, mwn);
+        }
         ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar + B_SF);  // S buffer free: the next S MMA overlaps this round
         // mask (only partially valid groups) and row max of the raw logits
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -309,16 +326,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         // final normalisation.
         const bool need = mx2 > m_ref + 8.f;
         if (__any_sync(0xffffffffu, need && m_ref != -INFINITY)) {
-          // O holds PV_{j-1}, complete (S_j was issued after it)
+          if (kv > 0) ptx::mbar_wait(bar + B_PF, (kv - 1) & 1);  // O holds PV_{kv-1}
+          ptx::tc_fence_after();
           const float f = need && m_ref != -INFINITY ? ptx::ex2(m_ref - mx2) : 1.f;
 #pragma unroll 1
           for (int c0 = 0; c0 < D; c0 += 16) {
             uint32_t ov[16];
-            NA_TMEM_LD16(trow + o_col + c0, ov);
+            NA_TMEM_LD16(trow + kColO + c0, ov);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int c = 0; c < 16; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * f);
-            NA_TMEM_ST16(trow + o_col + c0, ov);
+            NA_TMEM_ST16(trow + kColO + c0, ov);
           }
           l *= f;
         } else if (need) {
@@ -353,13 +371,17 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
-        // P over the first n_kv / 2 columns of the S buffer (already read)
-        NA_TMEM_ST32(trow, sv);
-        if (wide) NA_TMEM_ST32(trow + 32, (sv + 32));
+        // P into its buffer once PV_{kv-1} has read the previous P
+        if (kv > 0) ptx::mbar_wait(bar + B_PF, (kv - 1) & 1);
+        ptx::tc_fence_after();
+        NA_TMEM_ST32(trow + kColP, sv);
+        if (wide) NA_TMEM_ST32(trow + kColP + 32, (sv + 32));
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar + B_P);
         if (tracer) NA_TRACE_EV(2, tr, 21);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mw[i] = mwn[i];
       }
       // ---- epilogue: O / l, LSE (overlaps the next tile's S MMAs) ----
       // All MMAs of the tile are complete once O is final, so the tile's Q
@@ -367,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       // swizzle) and write it with one TMA store, which also clips rows past
       // a ragged class end.  The buffer returns to the producer (B_QE) once
       // the store has read it.
-      ptx::mbar_wait(bar + B_OF + ob, (ti >> 1) & 1);
+      ptx::mbar_wait(bar + B_OF, ti & 1);
       ptx::tc_fence_after();
       if (tracer) NA_TRACE_EV(2, tr, 22);
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -376,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t ov[32];
-        NA_TMEM_LD32(trow + o_col + c0, ov);
+        NA_TMEM_LD32(trow + kColO + c0, ov);
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < 32; c += 8)
@@ -387,7 +409,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                          pack2<BF16>(__uint_as_float(ov[c + 6]) * inv, __uint_as_float(ov[c + 7]) * inv));
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(bar + B_OE + ob);  // O buffer may be overwritten by tile ti + 2
+      // O is free again once every thread's loads are done: the next tile's
+      // PV_0 needs P_0, which these threads write after this point.
       if (tracer) NA_TRACE_EV(2, tr, 23);
       ptx::fence_proxy_async();           // staged O visible to the TMA engine
       ptx::named_bar_sync(1, kSoftmax);
