@@ -42,7 +42,7 @@ namespace na {
 namespace {
 
 #ifdef NA_TRACE
-static __device__ int g_trace_sel;  // trace build: 1 = dK/dV kernel, 0 = dQ kernel
+static __constant__ int g_trace_sel;  // trace build: 1 = dK/dV kernel, 0 = dQ kernel
 #define NA_BWD_TRACE_ON (g_trace_sel == (KV_STATIONARY ? 1 : 0))
 #else
 #define NA_BWD_TRACE_ON false
@@ -506,6 +506,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
           NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
           ptx::tmem_ld_wait();
+          if (tracer) NA_TRACE_EV(2 + grp, tr, 26 + 2 * gq);
           if (gq == 1) {
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar + B_SF + (gu & 1));
@@ -560,6 +561,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           } else {
             NA_TMEM_ST16(pk + 16 * gq, pk_s[gq]);       // dS -> A of dQ += dS K
           }
+          if (tracer) NA_TRACE_EV(2 + grp, tr, 27 + 2 * gq);
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();

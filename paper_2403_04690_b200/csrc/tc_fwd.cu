@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           r.chunk_mask(pl, org, mwn);
         }
         ptx::tmem_ld_wait();
+        if (tracer) NA_TRACE_EV(2, tr, 24);
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar + B_SF);  // S buffer free: the next S MMA overlaps this round
         // mask (only partially valid groups) and row max of the raw logits
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                                          __uint_as_float(sv[32 * gq + c + 4 + i])));
         }
         const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        if (tracer) NA_TRACE_EV(2, tr, 25);
         const float mx2 = mx * sl2;  // log2-domain max (-inf stays -inf)
         // lazy rescaling: move the reference max only when it grows by > 8
         // (factor 256); P stays <= 2^8 and the result is exact after the
@@ -371,8 +373,10 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
+        if (tracer) NA_TRACE_EV(2, tr, 26);
         // P into its buffer once PV_{kv-1} has read the previous P
         if (kv > 0) ptx::mbar_wait(bar + B_PF, (kv - 1) & 1);
+        if (tracer) NA_TRACE_EV(2, tr, 27);
         ptx::tc_fence_after();
         NA_TMEM_ST32(trow + kColP, sv);
         if (wide) NA_TMEM_ST32(trow + kColP + 32, (sv + 32));
@@ -449,7 +453,12 @@ cudaError_t launch(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* 
   }
   const long long tiles = (long long)g.BH * pl.nres * pl.tiles;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  const unsigned grid = (unsigned)(tiles < 2LL * num_sms() ? tiles : 2LL * num_sms());
+#ifdef NA_FWD_CTAS_PER_SM  // experiment knob (A/B builds only)
+  const long long per = NA_FWD_CTAS_PER_SM;
+#else
+  const long long per = 2;
+#endif
+  const unsigned grid = (unsigned)(tiles < per * num_sms() ? tiles : per * num_sms());
   prof_begin(KID_FWD_TC, st);
   kern<<<grid, kThreads, smem, st>>>(maps, g, pl, lse, (unsigned)tiles);
   prof_end(st);

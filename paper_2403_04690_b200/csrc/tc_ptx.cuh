@@ -331,7 +331,7 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
 // timeline studies; never in libna.so): per-CTA, per-role clock64 events.
 #ifdef NA_TRACE
 namespace na {
-static __device__ unsigned long long* g_trace;  // [ctas][4 roles][kTraceSlots], per TU
+static __constant__ unsigned long long* g_trace;  // [ctas][4 roles][kTraceSlots], per TU (constant: cached)
 constexpr int kTraceSlots = 256;
 constexpr int kTraceCtas = 64;
 __device__ __forceinline__ void trace(int role, int& idx, int tag) {
