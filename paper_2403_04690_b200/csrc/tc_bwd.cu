@@ -464,14 +464,17 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       unsigned tile_n = num_tiles;
       bool tn_known = false;
       float nrow_nl2 = 0.f, nrow_d = 0.f;
+      // This group's sub-chunks u_first, u_first + 2, ...: chunk origins by
+      // odometer (one chunk per step when a chunk has two sub-chunks, two
+      // otherwise); each mask is computed in the previous sub-chunk's load shadow.
+      int org[3] = {t.lo[0], t.lo[1], t.lo[2]};
+      if (u_first / ns) t.next_origin(pl, org);
+      uint32_t w[2];
+      r.sub_mask(pl, org, u_first % ns, w);
       for (int u = u_first; u < nsub; u += 2) {
         if (issuer && u != u_first) release_store();  // the store has had a sub-chunk to read
         const uint32_t gu = ub + u;
         const int j = u / ns, h = u % ns;
-        int org[3];
-        t.chunk_origin(pl, j, org);
-        uint32_t w[2];
-        r.sub_mask(pl, org, h, w);
         // Partner (query) values of the chunk, TMA-loaded with it:
         // [-LSE*log2(e) x 128 | D x 128] (cp.async-gathered); this sub-chunk's 64 columns.
         const uint32_t kv = kv_base + j;
@@ -499,12 +502,18 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         // S/dP buffer is released (B_SF) so the sub-chunk two ahead can start.
         const uint32_t pk = trow + kColPk + buf;
         uint32_t pk_p[2][16], pk_s[2][16];
+        uint32_t wn[2] = {0u, 0u};
 #pragma unroll
         for (int gq = 0; gq < 2; ++gq) {
           const bool any = __any_sync(0xffffffffu, w[gq] != 0u);
           uint32_t sv[32], pv[32];  // loaded unconditionally (a conditional load costs register zero-fills)
           NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
           NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
+          if (gq == 0 && u + 2 < nsub) {  // next sub-chunk's mask, in the load shadow
+            t.next_origin(pl, org);
+            if (ns == 1) t.next_origin(pl, org);
+            r.sub_mask(pl, org, h, wn);
+          }
           ptx::tmem_ld_wait();
           if (tracer) NA_TRACE_EV(2 + grp, tr, 26 + 2 * gq);
           if (gq == 1) {
@@ -567,6 +576,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar + B_P + (gu & 1));
         if (tracer) NA_TRACE_EV(2 + grp, tr, 21);
+        w[0] = wn[0];
+        w[1] = wn[1];
         if constexpr (!KV_STATIONARY) {
           if (pend) {  // previous tile's dQ, now that the tensor core has this sub-chunk
             epilogue(tp, ti - 1);
