@@ -296,18 +296,27 @@ struct RowCtx {
         const unsigned long long rep_hi = xm * pl.rep_hi | (pl.rep_sh ? xm >> pl.rep_sh : 0ull);
         if constexpr (RANK == 2) {
           range128(ylo * cx, (yhi + 1) * cx - 1, rlo, rhi);
+          rlo &= rep_lo;
+          rhi &= rep_hi;
         } else {
           const int c1 = pl.ckv[1];
           const int tlo = max(wlo[0] - org[0], 0), thi = min(whi[0] - org[0], pl.ckv[0] - 1);
-          if (ylo == 0 && yhi == c1 - 1) {  // whole y extent: one interval of rows
-            if (tlo <= thi) range128(tlo * c1 * cx, (thi + 1) * c1 * cx - 1, rlo, rhi);
-          } else {
-            for (int lt = tlo; lt <= thi; ++lt)
-              range128((lt * c1 + ylo) * cx, (lt * c1 + yhi + 1) * cx - 1, rlo, rhi);
+          if (pl.ckv[0] == 1) {  // one outermost slice: the rank-2 pattern if it is inside
+            if (tlo <= thi) range128(ylo * cx, (yhi + 1) * cx - 1, rlo, rhi);
+            rlo &= rep_lo;
+            rhi &= rep_hi;
+          } else if (tlo <= thi) {
+            // one slice's (y, x) pattern, then replicated over the slices
+            const int S = c1 * cx;
+            const unsigned long long slice =
+                (xm * pl.rep1) & lowbits64((yhi + 1) * cx) & ~lowbits64(ylo * cx);
+            const unsigned long long f_lo = slice * pl.rep2_lo;
+            const unsigned long long f_hi = slice * pl.rep2_hi | (pl.rep2_sh ? slice >> pl.rep2_sh : 0ull);
+            range128(tlo * S, (thi + 1) * S - 1, rlo, rhi);
+            rlo &= f_lo;
+            rhi &= f_hi;
           }
         }
-        rlo &= rep_lo;
-        rhi &= rep_hi;
       }
       mw[0] = (uint32_t)rlo;
       mw[1] = (uint32_t)(rlo >> 32);

@@ -154,6 +154,18 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows) {
       else if (b < 128) pl.rep_hi |= 1ull << (b - 64);
       if (b < 64 && b + cx > 64) pl.rep_sh = 64 - b;
     }
+    pl.rep1 = pl.rep2_lo = pl.rep2_hi = 0ull;
+    pl.rep2_sh = 0;
+    if (g.rank == 3 && pl.ckv[0] > 1) {
+      const int S = pl.ckv[1] * cx;  // <= 64 (rows_kv <= 128, ckv[0] >= 2)
+      for (int y = 0; y < pl.ckv[1]; ++y) pl.rep1 |= 1ull << (y * cx);
+      for (int t = 0; t < pl.ckv[0]; ++t) {
+        const int b = t * S;
+        if (b < 64) pl.rep2_lo |= 1ull << b;
+        else if (b < 128) pl.rep2_hi |= 1ull << (b - 64);
+        if (b < 64 && b + S > 64) pl.rep2_sh = 64 - b;
+      }
+    }
   }
   pl.f_tiles = make_fastdiv(pl.tiles);
   pl.f_nres = make_fastdiv(pl.nres);

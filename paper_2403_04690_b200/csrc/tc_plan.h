@@ -55,6 +55,12 @@ struct TcPlan {
   // every row (the copies never overlap, so the product has no carries).
   unsigned long long rep_lo, rep_hi;
   int rep_sh;
+  // Rank 3 with several outermost slices per chunk (ckv[0] > 1, so one slice
+  // of S = ckv[1] * ckv[2] bits fits 64): rep1 = sum over y of 2^(y*cx)
+  // builds one slice's pattern; rep2 = sum over t of 2^(t*S) (two halves and
+  // the straddle shift, as above) replicates it over the slices.
+  unsigned long long rep1, rep2_lo, rep2_hi;
+  int rep2_sh;
 };
 
 }  // namespace na
