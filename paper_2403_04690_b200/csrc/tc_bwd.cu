@@ -21,10 +21,10 @@
 // buffered, 4-stage ring of streamed chunks + their row vectors); warp 9
 // TMEM owner + OUT-MMA issuer; warp 10 S/dP-MMA issuer (one elected lane
 // each).  Sub-chunk gu (64 partner columns) is processed by warpgroup gu%2:
-//   S/dP(gu) -> TMEM buffer gu%2; the warpgroup loads it (B_SF releases the
-//   buffer, so S/dP(gu+2) overlaps this softmax), computes P and dS, writes
-//   them packed to their own TMEM buffer gu%2 (B_P), and the OUT warp issues
-//   the accumulating MMAs in order (B_PE frees the packed buffer).
+//   S/dP(gu) -> TMEM buffer gu%3; the warpgroup loads it, computes P and dS,
+//   writes them packed over the columns it has read (B_P), and the OUT warp
+//   issues the accumulating MMAs in order; their completion (B_PE) frees the
+//   buffer for S/dP(gu+3).  No warpgroup ever waits for an OUT MMA.
 // dK|dV share one 128-column accumulator drained at each tile start by the
 // warpgroup not owning the tile's first sub-chunk; dQ's is double-buffered.
 // Outputs are staged in the tile's dead stationary smem and TMA-stored.
@@ -70,24 +70,25 @@ struct BwdSmem {
   static constexpr int kBytes = kBar + 256;
 };
 
-// TMEM columns (512): [0,128) two 64-column S buffers and [128,256) two dP
-// buffers, each released (B_SF) as soon as its warpgroup has loaded it, so the
-// MMAs of the sub-chunk two ahead overlap this one's softmax; [256,384) two
-// packed-operand buffers (16-bit pairs: P^T at +0, dS^T at +32; dQ: dS at
-// +0), read by the OUT MMAs; [384,512) output accumulators: dK | dV (2D
-// columns, single-buffered when 2D = 128) or dQ (D columns, double-buffered).
-constexpr uint32_t kColS = 0, kColP = 128, kColPk = 256, kColOut = 384;
+// TMEM columns (512): three sub-chunk buffers b = gu % 3 at [128b, 128b + 128):
+// S at +0 and dP at +64 (64 partner columns each, fp32); the compute warps
+// write P^T (dQ: nothing) over S's first 32 columns and dS^T (dQ: dS) over
+// dP's, as packed 16-bit pairs, the A operands of the OUT MMAs.  A buffer is
+// reused for sub-chunk gu + 3 once gu's OUT MMAs are done (B_PE), so the S/dP
+// MMAs run up to three sub-chunks ahead.  [384,512) output accumulators:
+// dK | dV (2D columns, single-buffered when 2D = 128) or dQ (D columns,
+// double-buffered).
+constexpr uint32_t kColOut = 384;
 
 enum : int {
   B_AF = 0,                 // stationary tiles full [2]
   B_AE = B_AF + 2,          // stationary tiles empty [2] (the TMA-store issuer, after the read)
   B_B = B_AE + 2,           // streamed stage full [kStages]
   B_E = B_B + kStages,      // streamed stage empty [kStages]
-  B_S = B_E + kStages,      // S and dP of a sub-chunk ready [2]
-  B_SF = B_S + 2,           // S and dP buffers loaded by the warpgroup [2] (128 arrivals)
-  B_P = B_SF + 2,           // packed operands written [2] (128 arrivals)
-  B_PE = B_P + 2,           // packed operands consumed by the OUT MMAs [2]
-  B_OF = B_PE + 2,          // outputs of a tile final [2]
+  B_S = B_E + kStages,      // S and dP of a sub-chunk ready [3] (TMEM buffer gu % 3)
+  B_P = B_S + 3,            // P / dS written in place over that buffer [3] (128 arrivals)
+  B_PE = B_P + 3,           // OUT MMAs of the buffer's sub-chunk done: buffer free [3]
+  B_OF = B_PE + 3,          // outputs of a tile final [2]
   B_OE = B_OF + 2,          // outputs drained [2]
   B_COUNT = B_OE + 2
 };
@@ -125,12 +126,13 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(bar + B_AF + b, 1);
       ptx::mbar_init(bar + B_AE + b, 1);
-      ptx::mbar_init(bar + B_S + b, 1);
-      ptx::mbar_init(bar + B_SF + b, 128);
-      ptx::mbar_init(bar + B_P + b, 128);
-      ptx::mbar_init(bar + B_PE + b, 1);
       ptx::mbar_init(bar + B_OF + b, 1);
       ptx::mbar_init(bar + B_OE + b, KV_STATIONARY ? 128 : kCompute);
+    }
+    for (int b = 0; b < 3; ++b) {
+      ptx::mbar_init(bar + B_S + b, 1);
+      ptx::mbar_init(bar + B_P + b, 128);
+      ptx::mbar_init(bar + B_PE + b, 1);
     }
     for (int s = 0; s < kStages; ++s) {
       // dK/dV: + one cp.async arrival per producer lane (row-vector gather)
@@ -239,8 +241,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   } else if (warp == kMmaWarp || warp == kSWarp) {
     // ============ MMA issuers (whole warps, one elected lane issues) ============
     // Two independent in-order streams, so neither blocks the other: warp
-    // kSWarp issues S/dP of sub-chunk c once its TMEM buffer is free (B_SF of
-    // c-2) and its operands are resident; warp kMmaWarp issues OUT(k) once
+    // kSWarp issues S/dP of sub-chunk c once its TMEM buffer is free (B_PE of
+    // c-3) and its operands are resident; warp kMmaWarp issues OUT(k) once
     // sub-chunk k's packed operands are written.  A commit tracks the MMAs of
     // its own issuing thread: B_S (S warp); B_PE, B_E, B_OF (OUT warp) -- the
     // S/dP MMAs of a chunk are complete before its last OUT is issued (the
@@ -264,7 +266,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         for (int c_u = 0; c_u < nsub; ++c_u) {
           const uint32_t kv = c_kv + c_u / ns, gu = c_ub + c_u;
           const int h = c_u % ns, s = kv % kStages;
-          if (gu >= 2) ptx::mbar_wait(bar + B_SF + (gu & 1), ((gu >> 1) - 1) & 1);  // buffer loaded
+          const uint32_t b3 = gu % 3, r3 = gu / 3;
+          if (gu >= 3) ptx::mbar_wait(bar + B_PE + b3, (r3 - 1) & 1);  // buffer's previous OUT done
           if (c_u == 0) ptx::mbar_wait(bar + B_AF + ab, (c_ti >> 1) & 1);
           if (h == 0) ptx::mbar_wait(bar + B_B + s, (kv / kStages) & 1);
           ptx::tc_fence_after();
@@ -272,16 +275,16 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
           const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
           const uint32_t id = h ? idesc_s1 : idesc_s0;
-          const uint32_t buf = (gu & 1) * 64;
+          const uint32_t buf = b3 * 128;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
-            ptx::mma_ss_w(tmem + kColS + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
+            ptx::mma_ss_w(tmem + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
                           ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
-            ptx::mma_ss_w(tmem + kColP + buf, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
+            ptx::mma_ss_w(tmem + buf + 64, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
                           ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
           }
-          ptx::mma_commit_w(bar + B_S + (gu & 1));
+          ptx::mma_commit_w(bar + B_S + b3);
         }
         c_kv += ct.nchunks;
         c_ub += nsub;
@@ -304,8 +307,9 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           const uint32_t off = h * 64 * S::kRowBytes;
           const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
           const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
-          const uint32_t pk = tmem + kColPk + (gu & 1) * 64;
-          ptx::mbar_wait(bar + B_P + (gu & 1), (gu >> 1) & 1);
+          const uint32_t b3 = gu % 3;
+          const uint32_t pk = tmem + b3 * 128;  // P^T over S, dS^T over dP (in place)
+          ptx::mbar_wait(bar + B_P + b3, (gu / 3) & 1);
           if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 11);
           if (u == 0) {  // the tile's first OUT MMA overwrites the output buffer: drained?
             if (kOutDouble) {
@@ -322,15 +326,15 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
               // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
               ptx::mma_ts_w(tmem + out + D, pk + kk * 8,
                             ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
-              ptx::mma_ts_w(tmem + out, pk + 32 + kk * 8,
+              ptx::mma_ts_w(tmem + out, pk + 64 + kk * 8,
                             ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
             } else {
               // dQ += dS K
-              ptx::mma_ts_w(tmem + out, pk + kk * 8,
+              ptx::mma_ts_w(tmem + out, pk + 64 + kk * 8,
                             ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
             }
           }
-          ptx::mma_commit_w(bar + B_PE + (gu & 1));
+          ptx::mma_commit_w(bar + B_PE + b3);
           if (h == ns - 1) ptx::mma_commit_w(bar + B_E + s);
           if (u == nsub - 1) ptx::mma_commit_w(bar + B_OF + ob);
           if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 12);
@@ -488,9 +492,10 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
             if constexpr (!KV_STATIONARY) row_vals(tn, rn, nrow_nl2, nrow_d);
           }
         }
-        const uint32_t buf = (gu & 1) * 64;
+        const uint32_t b3 = gu % 3;
+        const uint32_t buf = b3 * 128;  // S at +0, dP at +64; P / dS written back in place
         if (tracer) NA_TRACE_EV(2 + grp, tr, 19);
-        ptx::mbar_wait(bar + B_S + (gu & 1), (gu >> 1) & 1);
+        ptx::mbar_wait(bar + B_S + b3, (gu / 3) & 1);
         if constexpr (KV_STATIONARY) {
           // The chunk's stage is still held (its B_E needs this P), so its
           // phase is current: the row-vector bytes are visible after this.
@@ -498,17 +503,18 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         }
         if (tracer) NA_TRACE_EV(2 + grp, tr, 20);
         ptx::tc_fence_after();
-        // Per 32-column half: load S and dP; after the second half's load the
-        // S/dP buffer is released (B_SF) so the sub-chunk two ahead can start.
-        const uint32_t pk = trow + kColPk + buf;
+        // Per 32-column half: load S and dP, compute P and dS, and store them
+        // packed over the columns already read (the buffer stays this
+        // sub-chunk's until its OUT MMAs are done; three buffers rotate).
+        const uint32_t pk = trow + buf;
         uint32_t pk_p[2][16], pk_s[2][16];
         uint32_t wn[2] = {0u, 0u};
 #pragma unroll
         for (int gq = 0; gq < 2; ++gq) {
           const bool any = __any_sync(0xffffffffu, w[gq] != 0u);
           uint32_t sv[32], pv[32];  // loaded unconditionally (a conditional load costs register zero-fills)
-          NA_TMEM_LD32(trow + kColS + buf + 32 * gq, sv);
-          NA_TMEM_LD32(trow + kColP + buf + 32 * gq, pv);
+          NA_TMEM_LD32(trow + buf + 32 * gq, sv);
+          NA_TMEM_LD32(trow + buf + 64 + 32 * gq, pv);
           if (gq == 0 && u + 2 < nsub) {  // next sub-chunk's mask, in the load shadow
             t.next_origin(pl, org);
             if (ns == 1) t.next_origin(pl, org);
@@ -516,13 +522,6 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           }
           ptx::tmem_ld_wait();
           if (tracer) NA_TRACE_EV(2 + grp, tr, 26 + 2 * gq);
-          if (gq == 1) {
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(bar + B_SF + (gu & 1));
-          } else if (gu >= 2) {
-            ptx::mbar_wait(bar + B_PE + (gu & 1), ((gu >> 1) - 1) & 1);  // packed buffer free
-            ptx::tc_fence_after();
-          }
           if (!any) {
 #pragma unroll
             for (int c = 0; c < 16; ++c) pk_p[gq][c] = pk_s[gq][c] = 0u;
@@ -566,15 +565,15 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           }
           if constexpr (KV_STATIONARY) {
             NA_TMEM_ST16(pk + 16 * gq, pk_p[gq]);       // P^T  -> A of dV += P^T dO
-            NA_TMEM_ST16(pk + 32 + 16 * gq, pk_s[gq]);  // dS^T -> A of dK += dS^T Q
+            NA_TMEM_ST16(pk + 64 + 16 * gq, pk_s[gq]);  // dS^T -> A of dK += dS^T Q
           } else {
-            NA_TMEM_ST16(pk + 16 * gq, pk_s[gq]);       // dS -> A of dQ += dS K
+            NA_TMEM_ST16(pk + 64 + 16 * gq, pk_s[gq]);  // dS -> A of dQ += dS K
           }
           if (tracer) NA_TRACE_EV(2 + grp, tr, 27 + 2 * gq);
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(bar + B_P + (gu & 1));
+        ptx::mbar_arrive(bar + B_P + b3);
         if (tracer) NA_TRACE_EV(2 + grp, tr, 21);
         w[0] = wn[0];
         w[1] = wn[1];
