@@ -86,8 +86,9 @@ def lib():
             L.nar_contains.argtypes = [P, i64, i64]
             L.nar_fwd.argtypes = [P, ctypes.c_int, vp, vp, vp, dp, dp]
             L.nar_fwd_tokens.argtypes = [P, ctypes.c_int, vp, vp, vp, i64, vp, dp, dp]
-            L.nar_bwd.argtypes = [P, ctypes.c_int, vp, vp, vp, vp, dp, dp, dp]
-            L.nar_bwd_tokens.argtypes = [P, ctypes.c_int, vp, vp, vp, vp, i64, vp, dp, dp, dp]
+            L.nar_bwd.argtypes = [P, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, dp, dp, dp]
+            L.nar_bwd_tokens.argtypes = [P, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, i64, vp, dp, dp,
+                                         dp]
             _lib = L
     return _lib
 
@@ -171,22 +172,28 @@ def fwd_tokens(p: Problem, q, k, v, tokens):
     return o, lse
 
 
-def bwd(p: Problem, q, k, v, d_o):
-    """Full backward.  Returns (dQ, dK, dV), each [B,H,N,D] fp64."""
+def bwd(p: Problem, q, k, v, d_o, stored_o: bool = False):
+    """Full backward.  Returns (dQ, dK, dV), each [B,H,N,D] fp64.
+
+    stored_o=False: the exact gradient.  stored_o=True: the softmax-Jacobian
+    term D_x = <dO_x, O_x> uses O as the method stores it -- the oracle's own
+    fp64 O rounded to the inputs' dtype (reading R12)."""
     (bq, bk, bv, bo), code = _prep(q, k, v, d_o)
     N, BH, D = _tokens(p), p.batch * p.heads, p.head_dim
     outs = [np.empty((BH * N * D,), np.float64) for _ in range(3)]
-    rc = lib().nar_bwd(ctypes.byref(p), code, bq[2], bk[2], bv[2], bo[2], *map(_ptr, outs))
+    rc = lib().nar_bwd(ctypes.byref(p), code, code if stored_o else F64, bq[2], bk[2], bv[2], bo[2],
+                       *map(_ptr, outs))
     if rc:
         raise ValueError(f"oracle rejected problem (code {rc})")
     return tuple(o.reshape(p.batch, p.heads, N, D) for o in outs)
 
 
-def bwd_tokens(p: Problem, q, k, v, d_o, tokens):
+def bwd_tokens(p: Problem, q, k, v, d_o, tokens, stored_o: bool = False):
     (bq, bk, bv, bo), code = _prep(q, k, v, d_o)
     t = np.ascontiguousarray(np.asarray(tokens, dtype=np.int64))
     outs = [np.empty((len(t), p.head_dim), np.float64) for _ in range(3)]
-    rc = lib().nar_bwd_tokens(ctypes.byref(p), code, bq[2], bk[2], bv[2], bo[2], len(t),
+    rc = lib().nar_bwd_tokens(ctypes.byref(p), code, code if stored_o else F64, bq[2], bk[2], bv[2],
+                              bo[2], len(t),
                               t.ctypes.data, *map(_ptr, outs))
     if rc:
         raise ValueError(f"oracle rejected problem (code {rc})")

@@ -222,8 +222,25 @@ int nar_fwd_tokens(const nar_problem* p, int dtype, const void* q, const void* k
   return 0;
 }
 
-int nar_bwd(const nar_problem* p, int dtype, const void* q, const void* k, const void* v,
-            const void* d_o, double* dq, double* dk, double* dv) {
+/* O as the method stores it (reading R12: D_x uses the stored output O, in
+ * the inputs' 16-bit dtype): the fp64 value rounded to fp32 (the kernel's
+ * accumulator) and then to o_dtype, round-to-nearest-even.  NAR_F64 = exact. */
+static double stored(int o_dtype, double x) {
+  if (o_dtype == NAR_F64) return x;
+  float f = (float)x;
+  if (o_dtype == NAR_F16) return (double)(_Float16)f;
+  if (o_dtype == NAR_BF16) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+    u &= 0xffff0000u;
+    memcpy(&f, &u, 4);
+  }
+  return (double)f;
+}
+
+int nar_bwd(const nar_problem* p, int dtype, int o_dtype, const void* q, const void* k,
+            const void* v, const void* d_o, double* dq, double* dk, double* dv) {
   int rc = nar_check(p);
   if (rc) return rc;
   const int64_t N = tokens_per_slice(p), BH = (int64_t)p->batch * p->heads;
@@ -243,7 +260,7 @@ int nar_bwd(const nar_problem* p, int dtype, const void* q, const void* k, const
       forward_row(p, dtype, q, k, v, bh, x, keys, prob, &nk, o_row);
       const int64_t xo = (bh * N + x) * D;
       double Dx = 0.0;                          /* D_x = <dO_x, O_x> */
-      for (int d = 0; d < D; ++d) Dx += load(dtype, d_o, xo + d) * o_row[d];
+      for (int d = 0; d < D; ++d) Dx += load(dtype, d_o, xo + d) * stored(o_dtype, o_row[d]);
       for (int j = 0; j < nk; ++j) {
         const int64_t yo = (bh * N + keys[j]) * D;
         double dP = 0.0;                        /* dP_xy = <dO_x, v_y> */
@@ -263,9 +280,9 @@ int nar_bwd(const nar_problem* p, int dtype, const void* q, const void* k, const
   return 0;
 }
 
-int nar_bwd_tokens(const nar_problem* p, int dtype, const void* q, const void* k, const void* v,
-                   const void* d_o, int64_t n, const int64_t* tokens, double* dq, double* dk,
-                   double* dv) {
+int nar_bwd_tokens(const nar_problem* p, int dtype, int o_dtype, const void* q, const void* k,
+                   const void* v, const void* d_o, int64_t n, const int64_t* tokens, double* dq,
+                   double* dk, double* dv) {
   int rc = nar_check(p);
   if (rc) return rc;
   const int64_t N = tokens_per_slice(p);
@@ -289,7 +306,7 @@ int nar_bwd_tokens(const nar_problem* p, int dtype, const void* q, const void* k
     {
       const int64_t xo = (bh * N + t) * D;
       double Dx = 0.0;
-      for (int d = 0; d < D; ++d) Dx += load(dtype, d_o, xo + d) * o_row[d];
+      for (int d = 0; d < D; ++d) Dx += load(dtype, d_o, xo + d) * stored(o_dtype, o_row[d]);
       for (int j = 0; j < nk; ++j) {
         const int64_t yo = (bh * N + keys[j]) * D;
         double dP = 0.0;
@@ -323,7 +340,7 @@ int nar_bwd_tokens(const nar_problem* p, int dtype, const void* q, const void* k
           const int64_t xo = (bh * N + x) * D, to = (bh * N + t) * D;
           double Dx = 0.0, dP = 0.0;
           for (int d = 0; d < D; ++d) {
-            Dx += load(dtype, d_o, xo + d) * o_row[d];
+            Dx += load(dtype, d_o, xo + d) * stored(o_dtype, o_row[d]);
             dP += load(dtype, d_o, xo + d) * load(dtype, v, to + d);
           }
           const double dS = prob[jt] * (dP - Dx);

@@ -70,13 +70,17 @@ int nar_fwd_tokens(const nar_problem* p, int dtype, const void* q, const void* k
                    const void* v, int64_t n, const int64_t* tokens,
                    double* o /* [n, D] */, double* lse /* [n] */);
 
-/* Full backward (scatter form).  Recomputes O and LSE internally in fp64. */
-int nar_bwd(const nar_problem* p, int dtype, const void* q, const void* k,
+/* Full backward (scatter form).  Recomputes O and LSE internally in fp64.
+ * o_dtype: NAR_F64 -> the exact gradient (D_x from the fp64 O); a 16-bit
+ * code -> D_x = <dO_x, O_x> with O as the method stores it, the fp64 O
+ * rounded to fp32 then to that dtype (reading R12).  The rounding
+ * is the oracle's own; no value from the GPU enters. */
+int nar_bwd(const nar_problem* p, int dtype, int o_dtype, const void* q, const void* k,
             const void* v, const void* d_o, double* dq, double* dk, double* dv);
 
 /* Backward at n selected flat token indices (gather form): dq of query t,
  * dk and dv of key t.  Each output is [n, D]. */
-int nar_bwd_tokens(const nar_problem* p, int dtype, const void* q, const void* k,
+int nar_bwd_tokens(const nar_problem* p, int dtype, int o_dtype, const void* q, const void* k,
                    const void* v, const void* d_o, int64_t n, const int64_t* tokens,
                    double* dq, double* dk, double* dv);
 

@@ -285,6 +285,35 @@ def test_forward_and_backward_match_dense_autograd(case):
     np.testing.assert_allclose(dv.reshape(B * H, N, D), vf.grad.numpy(), **tol)
 
 
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("case", CASES[:4])
+def test_stored_output_backward_matches_dense_formula(case, dt):
+    """Reading R12: with stored_o the softmax-Jacobian term uses O as the method
+    stores it (fp64 -> fp32 -> the inputs' 16-bit dtype, round to nearest
+    even).  Reference: torch fp64 dense masked attention, torch's own dtype
+    conversion of O, and the textbook gradient formulas (no oracle code)."""
+    extent, kernel, dil, causal = case
+    D, B, H = 6, 1, 2
+    q, k, v, do = (t.to(dt) for t in problem_inputs(extent, D, B, H, seed=80, with_do=True))
+    p = oracle.make_problem(B, H, extent, D, kernel, dil, causal, scale=0.41)
+    dq, dk, dv = oracle.bwd(p, q, k, v, do, stored_o=True)
+    N = int(np.prod(extent))
+    mask = torch.from_numpy(brute_mask(extent, kernel, dil, causal))
+    qf, kf, vf, dof = (t.double().reshape(B * H, N, D) for t in (q, k, v, do))
+    s = (0.41 * qf @ kf.transpose(-1, -2)).masked_fill(~mask, float("-inf"))
+    P = torch.softmax(s, dim=-1)
+    o_stored = (P @ vf).float().to(dt).double()
+    Dx = (dof * o_stored).sum(-1, keepdim=True)
+    dS = P * (dof @ vf.transpose(-1, -2) - Dx)
+    tol = dict(rtol=0, atol=1e-12)
+    np.testing.assert_allclose(dq.reshape(B * H, N, D), (0.41 * dS @ kf).numpy(), **tol)
+    np.testing.assert_allclose(dk.reshape(B * H, N, D), (0.41 * dS.transpose(-1, -2) @ qf).numpy(), **tol)
+    np.testing.assert_allclose(dv.reshape(B * H, N, D), (P.transpose(-1, -2) @ dof).numpy(), **tol)
+    # and the stored O differs from the exact one: the term is not a no-op
+    ex = oracle.bwd(p, q, k, v, do)[0]
+    assert np.abs(ex - dq).max() > 0
+
+
 @pytest.mark.parametrize("case", CASES[:4])
 def test_backward_matches_finite_differences(case):
     """Central differences (h = 1e-5) of L = <dO, O> through the oracle's own
