@@ -15,6 +15,7 @@
 
 #include "na_geom.cuh"
 #include "na_kernels.h"
+#include "tc_plan.h"
 
 namespace na {
 namespace {
@@ -146,37 +147,40 @@ __global__ void __launch_bounds__(256) fna_bwd_pre(Geom g, const T* __restrict__
 // token's index, writes the pair (-LSE_x * log2(e), D_x) into the two planes
 // of the class-compacted layout (na_geom.cuh, Geom::rv_*), so the backward
 // kernels fetch a chunk's partner values with one TMA box.
-__device__ __forceinline__ long long rv_index(const Geom& g, long long row) {
-  // 32-bit division (a 64-bit one is emulated and dominated this HBM-bound
-  // kernel); B*H*N < 2^32 for any problem whose tensors fit in memory.
-  const unsigned r32 = (unsigned)row;
-  const int bh = (int)(r32 / (unsigned)g.N);
-  const int n = (int)(r32 - (unsigned)bh * (unsigned)g.N);
-  int res = 0;
+// Divisors of the token -> (b*h, residue class, compacted coordinate) map
+// as multiply-high magic numbers (the integer divisions dominated this
+// HBM-bound kernel for multi-dimensional problems).
+struct RvDiv {
+  FastDiv n, l[3], dil[3];
+};
+
+__device__ __forceinline__ long long rv_index(const Geom& g, const RvDiv& f, long long row) {
+  // B*H*N < 2^31 for any problem whose tensors fit in memory (validated).
+  const uint32_t r32 = (uint32_t)row;
+  const uint32_t bh = fdiv(r32, f.n);
+  uint32_t n = r32 - bh * f.n.d;
+  int res = 0, mul = 1;
   long long off = 0;
-  if (g.rank == 1) {  // fast path: one division (none without dilation)
-    const int d = g.dil[0];
-    const int c = d == 1 ? n : n / d;
-    res = n - c * d;
-    off = c;
-  } else {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {  // constant indices: Geom stays in the param space
-      if (a < g.rank) {
-        const int x = (n / g.tstride[a]) % g.L[a];
-        res = res * g.dil[a] + x % g.dil[a];
-        off += (long long)(x / g.dil[a]) * g.rv_cs[a];
-      }
+  for (int a = 2; a >= 0; --a) {  // innermost axis first
+    if (a < g.rank) {
+      const uint32_t rest = fdiv(n, f.l[a]);
+      const uint32_t x = n - rest * f.l[a].d;
+      n = rest;
+      const uint32_t c = fdiv(x, f.dil[a]);
+      res += (int)(x - c * f.dil[a].d) * mul;
+      mul *= g.dil[a];
+      off += (long long)c * g.rv_cs[a];
     }
   }
-  return rv_base(g, bh, res) + off;
+  return rv_base(g, (int)bh, res) + off;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restrict__ o,
                                                        const T* __restrict__ d_o,
                                                        float* __restrict__ Dvec,
-                                                       const float* __restrict__ lse) {
+                                                       const float* __restrict__ lse, RvDiv f) {
   // D/8 threads per row; only the tensor-core path (D in {32, 64}) launches
   // this kernel, so tpr is a power of two: shift/mask, no 64-bit division.
   const int tpr = g.D / 8;
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restri
   long long i = 0;
   if (lse && part == 0 && valid) {
     l = lse[row];
-    i = rv_index(g, row);
+    i = rv_index(g, f, row);
   }
   float s = 0.f;
   if (valid) {
@@ -415,16 +419,22 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
       if (e != cudaSuccess) return e;
     }
   }
+  RvDiv f;
+  f.n = make_fastdiv((uint32_t)g.N);
+  for (int a = 0; a < 3; ++a) {
+    f.l[a] = make_fastdiv((uint32_t)(a < g.rank ? g.L[a] : 1));
+    f.dil[a] = make_fastdiv((uint32_t)(a < g.rank ? g.dil[a] : 1));
+  }
   prof_begin(KID_BWD_PRE, st);
   const unsigned vgrid = (unsigned)((rows * (g.D / 8) + 255) / 256);
   switch (dtype) {
     case 0: fna_bwd_pre<float><<<grid, 256, 0, st>>>(g, (const float*)o, (const float*)d_o, Dvec); break;
     case 1:
-      fna_bwd_pre_vec<__half><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec, lse);
+      fna_bwd_pre_vec<__half><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec, lse, f);
       break;
     default:
       fna_bwd_pre_vec<__nv_bfloat16><<<vgrid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
-                                                            (const __nv_bfloat16*)d_o, Dvec, lse);
+                                                            (const __nv_bfloat16*)d_o, Dvec, lse, f);
   }
   prof_end(st);
   return cudaGetLastError();
