@@ -111,7 +111,9 @@ size_t na_bwd_workspace_size(const na_problem* p);
 
 /* Backward.  Reads q, k, v, o, d_o (dL/dO) and lse from na_fwd on the same
  * inputs; writes dq, dk, dv (each element by exactly one thread; no
- * atomics).  `workspace` (device, >= na_bwd_workspace_size bytes) is
+ * atomics).  The softmax-Jacobian term D_x = <dO_x, O_x> is formed from the
+ * `o` passed in, i.e. the stored (dtype-rounded) forward output (DESIGN.md
+ * reading R12).  `workspace` (device, >= na_bwd_workspace_size bytes) is
  * scratch owned by the caller.  Three launches on `stream`:
  * D_x = <dO_x, O_x>, then dK/dV (key-stationary, inverse neighborhood map),
  * then dQ (query-stationary, forward map). */
