@@ -337,6 +337,17 @@ def per_config_table(args, world, rank, peaks):
             fwd()
             na.na_bwd(q, k, v, o, do, lse, dq=dq, dk=dk, dv=dv, workspace=ws, **kw)
 
+        # tile-plan tuning (setup, untimed): rank 0 measures the planner's
+        # candidates, every rank uses its picks (rank 0 decides)
+        pick = [0, 0, 0]
+        if rank == 0:
+            pick = list(na.na_tune(q, k, v, do, **kw))
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor(pick, dtype=torch.int32, device="cuda")
+            dist.broadcast(t, 0)
+            pick = t.tolist()
+        na.na_set_plan_choice(pr, pick)
         for _ in range(2):
             fwd_bwd()
         torch.cuda.synchronize()
@@ -354,6 +365,7 @@ def per_config_table(args, world, rank, peaks):
             "fwd_tensor_peak_frac": round(fl_f / (f_ms * 1e-3) / 1e12 / (world * peak_tf), 4),
             "fwd_bwd_tensor_peak_frac": round(fl_fb / (fb_ms * 1e-3) / 1e12 / (world * peak_tf), 4),
             "fwd_hbm_frac": round(fwd_bytes / (f_ms * 1e-3) / 1e9 / (world * peak_bw), 4),
+            "plan_pick": pick,
         }
         del q, k, v, do, o, lse, dq, dk, dv, ws
         torch.cuda.empty_cache()

@@ -121,6 +121,26 @@ na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* 
                  const void* o, const void* d_o, const float* lse, void* dq, void* dk,
                  void* dv, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Tile-plan tuning (tensor-core path).  The planner ranks tile / KV-chunk
+ * shapes with a cost model; na_tune runs the
+ * forward and backward with each of the na_plan_candidates(p) cheapest
+ * plans on the caller's buffers (all outputs are overwritten; inputs as for
+ * na_fwd / na_bwd), keeps the fastest plan per kernel (forward, dK/dV, dQ)
+ * in a process-wide table keyed by the problem's geometry, head_dim and
+ * dtype, and returns the picks in choice_out (may be NULL).  Synchronizes
+ * `stream`.  Later na_fwd / na_bwd calls with that geometry use the picks.
+ * Every plan computes the same result up to floating-point summation order.
+ * na_get/set_plan_choice read and set the picks directly (e.g. to broadcast
+ * rank 0's choice to the other ranks of a job); picks are in
+ * [0, na_plan_candidates(p)).  na_plan_candidates returns 1 for rank 1 and
+ * for the SIMT path, -1 for an invalid problem. */
+int na_plan_candidates(const na_problem* p);
+na_status na_tune(const na_problem* p, const void* q, const void* k, const void* v, void* o,
+                  float* lse, const void* d_o, void* dq, void* dk, void* dv, void* workspace,
+                  size_t workspace_bytes, void* stream, int32_t choice_out[3]);
+na_status na_get_plan_choice(const na_problem* p, int32_t choice[3]);
+na_status na_set_plan_choice(const na_problem* p, const int32_t choice[3]);
+
 /* Which kernel family na_fwd/na_bwd would run for `p` (NA_IMPL_SIMT or
  * NA_IMPL_TC), or -1 if `p` is invalid.  Host only. */
 int na_selected_impl(const na_problem* p);

@@ -269,6 +269,93 @@ na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* 
   return s;
 }
 
+int na_plan_candidates(const na_problem* p) {
+  if (validate(p) != NA_OK) return -1;
+  na::Geom g = make_geom(p);
+  const char* why;
+  if (select_impl(p, g, &why) != NA_IMPL_TC) return 1;
+  return na::tc_plan_candidates(g);
+}
+
+na_status na_get_plan_choice(const na_problem* p, int32_t choice[3]) {
+  na_status s = validate(p);
+  if (s != NA_OK) return s;
+  if (!choice) return fail(NA_ERR_NULL, "choice is NULL");
+  const na::PlanChoice c = na::plan_choice(make_geom(p), (int)p->dtype);
+  choice[0] = c.fwd;
+  choice[1] = c.dkdv;
+  choice[2] = c.dq;
+  g_last_error.clear();
+  return NA_OK;
+}
+
+na_status na_set_plan_choice(const na_problem* p, const int32_t choice[3]) {
+  na_status s = validate(p);
+  if (s != NA_OK) return s;
+  if (!choice) return fail(NA_ERR_NULL, "choice is NULL");
+  const int n = na_plan_candidates(p);
+  for (int i = 0; i < 3; ++i)
+    if (choice[i] < 0 || choice[i] >= n)
+      return fail(NA_ERR_SHAPE, "plan choice %d out of range [0, %d)", choice[i], n);
+  na::set_plan_choice(make_geom(p), (int)p->dtype, na::PlanChoice{choice[0], choice[1], choice[2]});
+  g_last_error.clear();
+  return NA_OK;
+}
+
+na_status na_tune(const na_problem* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                  const void* d_o, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                  void* stream, int32_t choice_out[3]) {
+  na_status s = validate(p);
+  if (s != NA_OK) return s;
+  const int n = na_plan_candidates(p);
+  int32_t best[3] = {0, 0, 0};
+  if (n > 1) {
+    // Time every candidate plan for each kernel (forward, dK/dV, dQ) with
+    // the launch-event hook, keep the fastest per kernel.  The caller's own
+    // profiling state is set aside meanwhile.
+    const bool prof_saved = g_prof;
+    std::vector<ProfEntry> list_saved;
+    list_saved.swap(g_prof_list);
+    float best_ms[3] = {1e30f, 1e30f, 1e30f};
+    for (int c = 0; c < n && s == NA_OK; ++c) {
+      const int32_t pick[3] = {c, c, c};
+      s = na_set_plan_choice(p, pick);
+      for (int it = 0; it < 3 && s == NA_OK; ++it) {
+        g_prof = it > 0;  // first pass warms up
+        s = na_fwd(p, q, k, v, o, lse, stream);
+        if (s == NA_OK)
+          s = na_bwd(p, q, k, v, o, d_o, lse, dq, dk, dv, workspace, workspace_bytes, stream);
+      }
+      g_prof = false;
+      float sum[3] = {0.f, 0.f, 0.f};
+      for (ProfEntry& e : g_prof_list) {
+        float t = 0.f;
+        if (cudaEventSynchronize(e.b) == cudaSuccess) cudaEventElapsedTime(&t, e.a, e.b);
+        const int slot = e.id == na::KID_FWD_TC ? 0 : e.id == na::KID_DKDV_TC ? 1 : e.id == na::KID_DQ_TC ? 2 : -1;
+        if (slot >= 0) sum[slot] += t;
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+      }
+      g_prof_list.clear();
+      for (int i = 0; i < 3; ++i)
+        if (sum[i] < best_ms[i]) {
+          best_ms[i] = sum[i];
+          best[i] = c;
+        }
+    }
+    g_prof = prof_saved;
+    g_prof_list.swap(list_saved);
+    if (s != NA_OK) return s;
+    s = na_set_plan_choice(p, best);
+    if (s != NA_OK) return s;
+  }
+  if (choice_out) {
+    for (int i = 0; i < 3; ++i) choice_out[i] = best[i];
+  }
+  g_last_error.clear();
+  return NA_OK;
+}
+
 const char* na_status_string(na_status s) {
   switch (s) {
     case NA_OK: return "ok";

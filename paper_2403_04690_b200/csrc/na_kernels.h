@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include "na_geom.cuh"
+#include "tc_plan.h"
 
 namespace na {
 
@@ -37,6 +38,11 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
 // tcgen05 path.  tc_supported() is a pure host check; the launchers return
 // cudaErrorNotSupported for problems outside it.
 bool tc_supported(int dtype, const Geom& g, const char** why);
+// Candidate plans of the tile planner for g (1 for rank 1), and the measured
+// choice per kernel (tc_host.cpp; na_tune sets it).
+int tc_plan_candidates(const Geom& g);
+PlanChoice plan_choice(const Geom& g, int dtype);
+void set_plan_choice(const Geom& g, int dtype, PlanChoice c);
 cudaError_t tc_fwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
                    void* o, float* lse, cudaStream_t st, int* launches);
 cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,

@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int RANK, int D, bool BF16>
-cudaError_t launch_both(const Geom& g, const TcPlan& pl, const BwdMaps& mkv, const BwdMaps& mq,
+cudaError_t launch_both(const Geom& g, const TcPlan* pls, const BwdMaps& mkv, const BwdMaps& mq,
                         const float* rv, cudaStream_t st) {
   const int smem = BwdSmem<D>::kBytes + 1024;
   auto kdkdv = fna_dkdv_tc<RANK, D, BF16>;
@@ -661,22 +661,24 @@ cudaError_t launch_both(const Geom& g, const TcPlan& pl, const BwdMaps& mkv, con
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const long long tiles = (long long)g.BH * pl.nres * pl.tiles;
-  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  const unsigned grid = (unsigned)(tiles < num_sms() ? tiles : num_sms());
+  const long long tiles_kv = (long long)g.BH * pls[0].nres * pls[0].tiles;
+  const long long tiles_q = (long long)g.BH * pls[1].nres * pls[1].tiles;
+  if (tiles_kv > 0x7fffffffLL || tiles_q > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const unsigned grid_kv = (unsigned)(tiles_kv < num_sms() ? tiles_kv : num_sms());
+  const unsigned grid_q = (unsigned)(tiles_q < num_sms() ? tiles_q : num_sms());
   prof_begin(KID_DKDV_TC, st);
-  kdkdv<<<grid, kThreads, smem, st>>>(mkv, g, pl, rv, (unsigned)tiles);
+  kdkdv<<<grid_kv, kThreads, smem, st>>>(mkv, g, pls[0], rv, (unsigned)tiles_kv);
   prof_end(st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   prof_begin(KID_DQ_TC, st);
-  kdq<<<grid, kThreads, smem, st>>>(mq, g, pl, rv, (unsigned)tiles);
+  kdq<<<grid_q, kThreads, smem, st>>>(mq, g, pls[1], rv, (unsigned)tiles_q);
   prof_end(st);
   return cudaGetLastError();
 }
 
 template <int RANK>
-cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const BwdMaps& mkv, const BwdMaps& mq,
+cudaError_t by_type(int dtype, const Geom& g, const TcPlan* pl, const BwdMaps& mkv, const BwdMaps& mq,
                     const float* rv, cudaStream_t st) {
   const bool bf = dtype == 2;
   if (g.D == 64)
@@ -695,7 +697,9 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   if (!tc_supported(dtype, g, &why)) return cudaErrorNotSupported;
   cudaError_t e = bwd_preprocess(dtype, g, o, d_o, lse, Dvec, st);  // row-vector layout
   if (e != cudaSuccess) return e;
-  TcPlan pl = make_plan(g, 128);
+  // Each kernel has its own plan (na_tune may measure different winners).
+  const PlanChoice pc = plan_choice(g, dtype);
+  const TcPlan pls[2] = {make_plan(g, 128, pc.dkdv), make_plan(g, 128, pc.dq)};
   // dK/dV kernel: stationary K, V tiles; streamed Q, dO chunks; outputs dK, dV.
   // dQ kernel: stationary Q, dO tiles; streamed K, V chunks; output dQ.
   BwdMaps mkv, mq;
@@ -703,20 +707,21 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   const void* chunk_src[2][2] = {{q, d_o}, {k, v}};
   BwdMaps* mm[2] = {&mkv, &mq};
   for (int w = 0; w < 2; ++w) {
+    const TcPlan& pl = pls[w];
     if ((e = make_map(&mm[w]->a0, dtype, g, tile_src[w][0], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
     if ((e = make_map(&mm[w]->a1, dtype, g, tile_src[w][1], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
     if ((e = make_map(&mm[w]->b0, dtype, g, chunk_src[w][0], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
     if ((e = make_map(&mm[w]->b1, dtype, g, chunk_src[w][1], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
   }
-  if ((e = make_map(&mkv.out0, dtype, g, dk, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&mkv.out1, dtype, g, dv, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&mq.out0, dtype, g, dq, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mkv.out0, dtype, g, dk, pls[0].tq, pls[0].q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mkv.out1, dtype, g, dv, pls[0].tq, pls[0].q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mq.out0, dtype, g, dq, pls[1].tq, pls[1].q_box_x)) != cudaSuccess) return e;
   mq.out1 = mq.out0;
   *launches = 3;
   switch (g.rank) {
-    case 1: return by_type<1>(dtype, g, pl, mkv, mq, Dvec, st);
-    case 2: return by_type<2>(dtype, g, pl, mkv, mq, Dvec, st);
-    default: return by_type<3>(dtype, g, pl, mkv, mq, Dvec, st);
+    case 1: return by_type<1>(dtype, g, pls, mkv, mq, Dvec, st);
+    case 2: return by_type<2>(dtype, g, pls, mkv, mq, Dvec, st);
+    default: return by_type<3>(dtype, g, pls, mkv, mq, Dvec, st);
   }
 }
 

@@ -14,7 +14,10 @@
 namespace na {
 
 // Host side (tc_host.cpp).
-TcPlan make_plan(const Geom& g, int tile_rows);
+// `pick`: which of the kTopPlans cheapest candidates of the cost model
+// (0 = cheapest); *ncand (if given) = how many exist (1 for rank 1).
+TcPlan make_plan(const Geom& g, int tile_rows, int pick = 0, int* ncand = nullptr);
+// (plan_choice / set_plan_choice: na_kernels.h)
 int num_sms();  // SMs of the current device (cached per device)
 cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base,
                      const int box[3], int box_x);

@@ -480,7 +480,7 @@ cudaError_t tc_fwd(int dtype, const Geom& g, const void* q, const void* k, const
                    float* lse, cudaStream_t st, int* launches) {
   const char* why;
   if (!tc_supported(dtype, g, &why)) return cudaErrorNotSupported;
-  TcPlan pl = make_plan(g, /*q_tile_rows=*/128);
+  TcPlan pl = make_plan(g, /*q_tile_rows=*/128, plan_choice(g, dtype).fwd);
   FwdMaps maps;
   cudaError_t e;
   if ((e = make_map(&maps.q, dtype, g, q, pl.tq, pl.q_box_x)) != cudaSuccess) return e;

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -47,7 +48,7 @@ int box_x_for(int ext, int dil) {
 
 namespace {
 
-TcPlan make_plan_uncached(const Geom& g, int tile_rows) {
+TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand) {
   TcPlan pl{};
   int Lmax[3];
   for (int a = 0; a < 3; ++a) {
@@ -56,6 +57,7 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows) {
   }
   pl.nres = 1;
   for (int a = 0; a < g.rank; ++a) pl.nres *= g.dil[a];
+  if (ncand) *ncand = 1;
   if (g.rank == 1) {
     pl.tq[0] = tile_rows;
     pl.ckv[0] = 128;
@@ -67,9 +69,19 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows) {
     // balanced extents (ceil(h / n) for n chunks); minimise the cost of the
     // softmax rounds per useful query row: chunks * (MMA columns + a fixed
     // per-round cost of kRoundCols columns).
-    constexpr int kRoundCols = 96;
+    // The kTopPlans cheapest candidates are kept; `pick` selects one of them
+    // (0 = the model's choice; na_tune measures the others).
+    // NA_ROUND_COLS overrides the per-round cost (calibration experiments).
+    const char* env_cols = getenv("NA_ROUND_COLS");
+    const int kRoundCols = env_cols ? atoi(env_cols) : 96;
+    const int pick = std::min(std::max(pick_in, 0), kTopPlans - 1);
     const int R = g.rank;
-    double best = 1e30;
+    struct Cand {
+      double cost;
+      int tq[3], ck[3];
+    };
+    Cand top[kTopPlans];
+    int ntop = 0;
     auto consider = [&](const int tq[3]) {
       int h[3] = {1, 1, 1}, valid_rows = 1;
       for (int a = 0; a < R; ++a) {
@@ -97,11 +109,17 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows) {
             int chunks = 1;
             for (int a = 0; a < R; ++a) chunks *= ceil_div(h[a], ck[a]);
             const double cost = (double)chunks * (round16(rows) + kRoundCols) / valid_rows;
-            if (cost < best) {
-              best = cost;
+            // keep the kTopPlans cheapest candidates, sorted
+            if (ntop < kTopPlans || cost < top[ntop - 1].cost) {
+              int i = ntop < kTopPlans ? ntop++ : kTopPlans - 1;
+              while (i > 0 && top[i - 1].cost > cost) {
+                top[i] = top[i - 1];
+                --i;
+              }
+              top[i].cost = cost;
               for (int a = 0; a < 3; ++a) {
-                pl.tq[a] = a < R ? tq[a] : 1;
-                pl.ckv[a] = a < R ? ck[a] : 1;
+                top[i].tq[a] = a < R ? tq[a] : 1;
+                top[i].ck[a] = a < R ? ck[a] : 1;
               }
             }
           }
@@ -121,6 +139,12 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows) {
           t[0] = tile_rows / (tx * ty);
           consider(t);
         }
+    }
+    if (ncand) *ncand = ntop;
+    const Cand& c = top[std::min(pick, ntop - 1)];
+    for (int a = 0; a < 3; ++a) {
+      pl.tq[a] = c.tq[a];
+      pl.ckv[a] = c.ck[a];
     }
     pl.q_box_x = pl.tq[R - 1];
     pl.kv_box_x = pl.ckv[R - 1];
@@ -174,35 +198,100 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows) {
 
 }  // namespace
 
-// Plans depend only on the geometry; the multi-dimensional search costs
-// ~1 ms, so plans are cached per process (small linear table, mutex).
-TcPlan make_plan(const Geom& g, int tile_rows) {
-  struct Entry {
-    int key[14];
-    TcPlan plan;
-  };
-  static std::mutex mu;
-  static std::vector<Entry> cache;
-  int key[14] = {g.rank, tile_rows};
+// Plans depend only on the geometry (and the candidate picked); the
+// multi-dimensional search costs ~1 ms, so plans are cached per process
+// (small linear table, mutex).
+namespace {
+struct PlanEntry {
+  int key[15];
+  TcPlan plan;
+  int ncand;
+};
+std::mutex g_plan_mu;
+std::vector<PlanEntry> g_plans;
+
+void geom_key(const Geom& g, int tile_rows, int* key) {
+  key[0] = g.rank;
+  key[1] = tile_rows;
   for (int a = 0; a < 3; ++a) {
     key[2 + a] = g.L[a];
     key[5 + a] = g.k[a];
     key[8 + a] = g.dil[a];
     key[11 + a] = g.causal[a];
   }
+}
+}  // namespace
+
+TcPlan make_plan(const Geom& g, int tile_rows, int pick, int* ncand) {
+  int key[15];
+  geom_key(g, tile_rows, key);
+  key[14] = pick;
   {
-    std::lock_guard<std::mutex> lk(mu);
-    for (const Entry& e : cache)
-      if (std::equal(key, key + 14, e.key)) return e.plan;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    for (const PlanEntry& e : g_plans)
+      if (std::equal(key, key + 15, e.key)) {
+        if (ncand) *ncand = e.ncand;
+        return e.plan;
+      }
   }
-  const TcPlan pl = make_plan_uncached(g, tile_rows);
-  std::lock_guard<std::mutex> lk(mu);
-  if (cache.size() >= 256) cache.erase(cache.begin());
-  Entry e;
-  std::copy(key, key + 14, e.key);
+  int nc = 1;
+  const TcPlan pl = make_plan_uncached(g, tile_rows, pick, &nc);
+  if (ncand) *ncand = nc;
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  if (g_plans.size() >= 512) g_plans.erase(g_plans.begin());
+  PlanEntry e;
+  std::copy(key, key + 15, e.key);
   e.plan = pl;
-  cache.push_back(e);
+  e.ncand = nc;
+  g_plans.push_back(e);
   return pl;
+}
+
+// Measured plan choices (na_tune / na_set_plan_choice), per geometry, head
+// dim and dtype; absent = the cost model's choice (0, 0, 0).
+namespace {
+struct ChoiceEntry {
+  int key[16];
+  PlanChoice c;
+};
+std::mutex g_choice_mu;
+std::vector<ChoiceEntry> g_choices;
+void choice_key(const Geom& g, int dtype, int* key) {
+  geom_key(g, 128, key);
+  key[14] = g.D;
+  key[15] = dtype;
+}
+}  // namespace
+
+PlanChoice plan_choice(const Geom& g, int dtype) {
+  int key[16];
+  choice_key(g, dtype, key);
+  std::lock_guard<std::mutex> lk(g_choice_mu);
+  for (const ChoiceEntry& e : g_choices)
+    if (std::equal(key, key + 16, e.key)) return e.c;
+  return PlanChoice{0, 0, 0};
+}
+
+void set_plan_choice(const Geom& g, int dtype, PlanChoice c) {
+  int key[16];
+  choice_key(g, dtype, key);
+  std::lock_guard<std::mutex> lk(g_choice_mu);
+  for (ChoiceEntry& e : g_choices)
+    if (std::equal(key, key + 16, e.key)) {
+      e.c = c;
+      return;
+    }
+  if (g_choices.size() >= 512) g_choices.erase(g_choices.begin());
+  ChoiceEntry e;
+  std::copy(key, key + 16, e.key);
+  e.c = c;
+  g_choices.push_back(e);
+}
+
+int tc_plan_candidates(const Geom& g) {
+  int n = 1;
+  make_plan(g, 128, 0, &n);
+  return n;
 }
 
 int num_sms() {

@@ -33,6 +33,13 @@ __device__ __forceinline__ uint32_t fmod_(uint32_t n, uint32_t q, const FastDiv&
 }
 #endif
 
+constexpr int kTopPlans = 4;  // planner candidates kept for measurement (na_tune)
+
+// Which candidate plan each tensor-core kernel uses.
+struct PlanChoice {
+  int fwd, dkdv, dq;
+};
+
 struct TcPlan {
   int tq[3];       // query tile extent per axis (power of two, product 128; 1 beyond rank)
   int tq_shift[3]; // log2(tq)

@@ -48,7 +48,8 @@ _lib = None
 
 EXPORTS = ("na_validate", "na_fwd", "na_bwd", "na_bwd_workspace_size", "na_selected_impl",
            "na_status_string", "na_last_error", "na_last_launch_count", "na_profile_enable",
-           "na_profile_collect", "na_kernel_name")
+           "na_profile_collect", "na_kernel_name", "na_plan_candidates", "na_tune",
+           "na_get_plan_choice", "na_set_plan_choice")
 
 
 def lib():
@@ -84,6 +85,15 @@ def lib():
         L.na_profile_collect.restype = ctypes.c_int
         L.na_kernel_name.argtypes = [ctypes.c_int]
         L.na_kernel_name.restype = ctypes.c_char_p
+        I3 = ctypes.c_int32 * 3
+        L.na_plan_candidates.argtypes = [P]
+        L.na_plan_candidates.restype = ctypes.c_int
+        L.na_tune.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, I3]
+        L.na_tune.restype = ctypes.c_int
+        L.na_get_plan_choice.argtypes = [P, I3]
+        L.na_get_plan_choice.restype = ctypes.c_int
+        L.na_set_plan_choice.argtypes = [P, I3]
+        L.na_set_plan_choice.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -195,3 +205,34 @@ def na_bwd(q, k, v, o, d_o, lse, kernel_size, dilation=None, is_causal=None, sca
                         _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace),
                         workspace.numel() * workspace.element_size(), _stream()))
     return dq, dk, dv
+
+
+def na_plan_candidates(p: Problem) -> int:
+    """How many tile plans na_tune would measure for `p` (1: nothing to tune)."""
+    return lib().na_plan_candidates(ctypes.byref(p))
+
+
+def na_get_plan_choice(p: Problem):
+    c = (ctypes.c_int32 * 3)()
+    _check(lib().na_get_plan_choice(ctypes.byref(p), c))
+    return tuple(c)
+
+
+def na_set_plan_choice(p: Problem, choice):
+    _check(lib().na_set_plan_choice(ctypes.byref(p), (ctypes.c_int32 * 3)(*choice)))
+
+
+def na_tune(q, k, v, d_o, kernel_size, dilation=None, is_causal=None, scale=None):
+    """Measure the planner's candidate tile plans for this problem (forward,
+    dK/dV and dQ separately) on scratch outputs and keep the fastest for later
+    calls with the same geometry.  Returns the picks (fwd, dkdv, dq)."""
+    p = _problem_from(q, kernel_size, dilation, is_causal, scale, "auto")
+    for t, n in ((k, "k"), (v, "v"), (d_o, "d_o")):
+        _need(t, q, n)
+    o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
+    lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
+    ws = torch.empty((max(na_bwd_workspace_size(p), 16) + 3) // 4, dtype=torch.float32, device=q.device)
+    c = (ctypes.c_int32 * 3)()
+    _check(lib().na_tune(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(d_o),
+                         _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel() * 4, _stream(), c))
+    return tuple(c)

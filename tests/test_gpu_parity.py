@@ -209,3 +209,38 @@ def test_baseline_config_sampled(na, name):
     assert excess(flat(dv)[bt].float().cpu(), rdv, dt) <= 0
     for t in (o, lse, dq, dk, dv):
         assert torch.isfinite(t).all()
+
+
+# ------------------------------------------------------- tile-plan tuning
+
+PLAN_CASES = [
+    ([16, 12, 12], [7, 7, 7], [1, 1, 1], [1, 0, 0], 64, torch.float16),
+    ([30, 44], [9, 13], [3, 2], [0, 1], 32, torch.bfloat16),
+]
+
+
+@pytest.mark.parametrize("ext,ker,dil,cau,D,dt", PLAN_CASES)
+def test_every_candidate_plan_matches_oracle(na, ext, ker, dil, cau, D, dt):
+    """Each of the planner's candidate tile/chunk shapes (what na_tune picks
+    from) computes the same result; then na_tune's pick is used."""
+    cfg = na_synth.small_config(ext, ker, dil, cau, head_dim=D, batch=1, heads=2, dtype=dt)
+    p = na.make_problem(1, 2, list(ext), D, ker, dil, [bool(c) for c in cau], dtype=dt)
+    n = na.na_plan_candidates(p)
+    assert n > 1
+    q, k, v, do = na_synth.make_inputs(cfg, salt=13)
+    op = oracle_problem(cfg)
+    ro, rlse = oracle.fwd(op, q, k, v)
+    rdq, rdk, rdv = oracle.bwd(op, q, k, v, do, stored_o=True)
+    shp = (1, 2, cfg.tokens, D)
+    picks = [(c, c, c) for c in range(n)]
+    qd, kd, vd, dod = (t.cuda() for t in (q, k, v, do))
+    picks.append(na.na_tune(qd, kd, vd, dod, ker, dil, [bool(c) for c in cau]))
+    for pick in picks:
+        na.na_set_plan_choice(p, pick)
+        o, lse, dq, dk, dv = run_gpu(na, cfg, q, k, v, do, "tc")
+        assert excess(o.reshape(shp), ro, dt) <= 0, pick
+        assert max_err(lse.reshape(shp[:-1]), rlse) <= LSE_TOL[dt], pick
+        assert excess(dq.reshape(shp), rdq, dt, grad_tol(dt)) <= 0, pick
+        assert excess(dk.reshape(shp), rdk, dt, grad_tol(dt)) <= 0, pick
+        assert excess(dv.reshape(shp), rdv, dt) <= 0, pick
+    na.na_set_plan_choice(p, (0, 0, 0))
