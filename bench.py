@@ -63,7 +63,7 @@ def algorithmic_bytes(cfg, kernel):
     return {
         "fna_fwd_tc": 4 * E * s + 4 * rows,            # Q,K,V read; O write; LSE write
         "fna_fwd_simt": 4 * E * s + 4 * rows,
-        "fna_bwd_pre": 2 * E * s + 4 * rows,           # O, dO read; D write
+        "fna_bwd_pre": 2 * E * s + 12 * rows,          # O, dO, LSE read; (-LSE log2 e, D) written
         "fna_dkdv_tc": 6 * E * s + 8 * rows,           # Q,K,V,dO read; dK,dV write; LSE,D read
         "fna_dkdv_simt": 6 * E * s + 8 * rows,
         "fna_dq_tc": 5 * E * s + 8 * rows,             # Q,K,V,dO read; dQ write; LSE,D read
@@ -427,6 +427,18 @@ def run_native(args, world, rank, local):
         except Exception:
             traffic = None
     shares = {n: round(v[0] / sum(x[0] for x in per_kernel.values()), 4) for n, v in per_kernel.items()}
+    # every kernel of the step against the HBM roofline (algorithmic bytes of
+    # config B_d1 per launch / average launch time)
+    per_kernel_roof = {}
+    for n, (tot, cnt) in per_kernel.items():
+        ms_avg = tot / cnt
+        key = "fna_bwd_pre" if n.startswith("fna_bwd_pre") else n
+        try:
+            gbs = algorithmic_bytes(cfg0, key) / (ms_avg * 1e-3) / 1e9
+        except KeyError:
+            continue
+        per_kernel_roof[n] = {"avg_launch_ms": round(ms_avg, 5), "achieved_gbs": round(gbs, 1),
+                              "hbm_frac": round(gbs / peak, 4)}
 
     # end-to-end through the public API with host buffers
     e2e = None
@@ -483,7 +495,7 @@ def run_native(args, world, rank, local):
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
                      "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src,
-                     "step_share": shares},
+                     "step_share": shares, "kernels": per_kernel_roof},
         "per_config": per_config,
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
