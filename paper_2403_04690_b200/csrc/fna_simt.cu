@@ -176,43 +176,56 @@ __device__ __forceinline__ long long rv_index(const Geom& g, const RvDiv& f, lon
   return rv_base(g, (int)bh, res) + off;
 }
 
-template <typename T>
+template <typename T, int kPreRows>
 __global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restrict__ o,
                                                        const T* __restrict__ d_o,
                                                        float* __restrict__ Dvec,
                                                        const float* __restrict__ lse, RvDiv f) {
   // D/8 threads per row; only the tensor-core path (D in {32, 64}) launches
   // this kernel, so tpr is a power of two: shift/mask, no 64-bit division.
+  // Each thread covers kPreRows rows (one per 256/tpr-row slab of the block),
+  // all loads issued before any arithmetic: more bytes in flight per thread
+  // (2 for rank 1; the multi-dimensional slot arithmetic prefers 1).
   const int tpr = g.D / 8;
   const int shift = __ffs(tpr) - 1;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t row = gid >> shift;
-  const int part = (int)(gid & (tpr - 1));
-  const bool valid = row < (int64_t)g.BH * g.N;
-  // Row-vector mode: LSE and the destination index first, so their latency
-  // overlaps the O/dO loads (one HBM round trip per warp, not two).
-  float l = 0.f;
-  long long i = 0;
-  if (lse && part == 0 && valid) {
-    l = lse[row];
-    i = rv_index(g, f, row);
+  const int64_t slab = 256 >> shift;  // rows per slab
+  const int64_t row0 = (int64_t)blockIdx.x * kPreRows * slab + (threadIdx.x >> shift);
+  const int part = (int)(threadIdx.x & (tpr - 1));
+  const int64_t rows = (int64_t)g.BH * g.N;
+  uint4 a[kPreRows], b[kPreRows];
+  float l[kPreRows];
+  long long i[kPreRows];
+#pragma unroll
+  for (int k = 0; k < kPreRows; ++k) {
+    const int64_t row = row0 + k * slab;
+    const bool valid = row < rows;
+    // Row-vector mode: LSE and the destination index first, so their latency
+    // overlaps the O/dO loads (one HBM round trip per warp, not two).
+    l[k] = 0.f;
+    i[k] = 0;
+    if (lse && part == 0 && valid) {
+      l[k] = lse[row];
+      i[k] = rv_index(g, f, row);
+    }
+    a[k] = valid ? __ldg(reinterpret_cast<const uint4*>(o + row * g.D) + part) : make_uint4(0, 0, 0, 0);
+    b[k] = valid ? __ldg(reinterpret_cast<const uint4*>(d_o + row * g.D) + part) : make_uint4(0, 0, 0, 0);
   }
-  float s = 0.f;
-  if (valid) {
-    const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + row * g.D) + part);
-    const uint4 b = __ldg(reinterpret_cast<const uint4*>(d_o + row * g.D) + part);
-    const T* ea = reinterpret_cast<const T*>(&a);
-    const T* eb = reinterpret_cast<const T*>(&b);
+#pragma unroll
+  for (int k = 0; k < kPreRows; ++k) {
+    const int64_t row = row0 + k * slab;
+    const T* ea = reinterpret_cast<const T*>(&a[k]);
+    const T* eb = reinterpret_cast<const T*>(&b[k]);
+    float s = 0.f;
 #pragma unroll
     for (int e = 0; e < 8; ++e) s = fmaf(ld_val(ea[e]), ld_val(eb[e]), s);
-  }
-  for (int off = 1; off < tpr; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (part == 0 && valid) {
-    if (lse) {
-      Dvec[i] = -l * 1.4426950408889634f;
-      Dvec[i + g.rv_plane] = s;
-    } else {
-      Dvec[row] = s;
+    for (int off = 1; off < tpr; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (part == 0 && row < rows) {
+      if (lse) {
+        Dvec[i[k]] = -l[k] * 1.4426950408889634f;
+        Dvec[i[k] + g.rv_plane] = s;
+      } else {
+        Dvec[row] = s;
+      }
     }
   }
 }
@@ -426,15 +439,21 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
     f.dil[a] = make_fastdiv((uint32_t)(a < g.rank ? g.dil[a] : 1));
   }
   prof_begin(KID_BWD_PRE, st);
-  const unsigned vgrid = (unsigned)((rows * (g.D / 8) + 255) / 256);
+  const int rpt = g.rank == 1 ? 2 : 1;  // rows per thread
+  const unsigned vgrid = (unsigned)((rows * (g.D / 8) + 256 * rpt - 1) / (256 * rpt));
   switch (dtype) {
     case 0: fna_bwd_pre<float><<<grid, 256, 0, st>>>(g, (const float*)o, (const float*)d_o, Dvec); break;
     case 1:
-      fna_bwd_pre_vec<__half><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec, lse, f);
+      if (rpt == 2) fna_bwd_pre_vec<__half, 2><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec, lse, f);
+      else fna_bwd_pre_vec<__half, 1><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec, lse, f);
       break;
     default:
-      fna_bwd_pre_vec<__nv_bfloat16><<<vgrid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
-                                                            (const __nv_bfloat16*)d_o, Dvec, lse, f);
+      if (rpt == 2)
+        fna_bwd_pre_vec<__nv_bfloat16, 2><<<vgrid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
+                                                                 (const __nv_bfloat16*)d_o, Dvec, lse, f);
+      else
+        fna_bwd_pre_vec<__nv_bfloat16, 1><<<vgrid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
+                                                                 (const __nv_bfloat16*)d_o, Dvec, lse, f);
   }
   prof_end(st);
   return cudaGetLastError();
