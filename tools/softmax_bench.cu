@@ -12,12 +12,12 @@
 
 using namespace na;
 
-template <int MASKED, int MODE>
-__global__ void __launch_bounds__(128, 2) rounds(unsigned long long* out, int iters, uint32_t wbits) {
+template <int MASKED, int MODE, int NG = 4>
+__global__ void __launch_bounds__(128, 1) rounds(unsigned long long* out, int iters, uint32_t wbits) {
   // MODE 0 full round; 1 loads + stores only; 2 + mask/max; 3 + exponentials without the max
   __shared__ uint32_t slot;
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-  if (warp == 0) ptx::tmem_alloc<256>(&slot);
+  if (warp == 0) ptx::tmem_alloc<(NG == 4 ? 256 : 128)>(&slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -30,10 +30,10 @@ __global__ void __launch_bounds__(128, 2) rounds(unsigned long long* out, int it
   for (int it = 0; it < iters; ++it) {
     bool live[4];
 #pragma unroll
-    for (int gq = 0; gq < 4; ++gq) live[gq] = __any_sync(0xffffffffu, mw[gq] != 0u);
+    for (int gq = 0; gq < NG; ++gq) live[gq] = __any_sync(0xffffffffu, mw[gq] != 0u);
     uint32_t sv[128];
 #pragma unroll
-    for (int gq = 0; gq < 4; ++gq)
+    for (int gq = 0; gq < NG; ++gq)
       if (live[gq]) NA_TMEM_LD32(trow + 32 * gq, (sv + 32 * gq));
     ptx::tmem_ld_wait();
 #ifndef MAXCH
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(128, 2) rounds(unsigned long long* out, int it
 #pragma unroll
     for (int i = 0; i < MAXCH; ++i) m4[i] = -INFINITY;
 #pragma unroll
-    for (int gq = 0; gq < 4; ++gq) {
+    for (int gq = 0; gq < NG; ++gq) {
       if (!live[gq] || MODE == 1 || MODE == 3) continue;
       const uint32_t w = mw[gq];
       if (!__all_sync(0xffffffffu, w == 0xffffffffu)) {
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(128, 2) rounds(unsigned long long* out, int it
     const float nmu = m_ref == -INFINITY ? 0.f : -m_ref;
     float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int gq = 0; gq < 4; ++gq) {
+    for (int gq = 0; gq < NG; ++gq) {
       if (MODE == 1 || MODE == 2) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) sv[16 * gq + c] ^= sv[32 * gq + c + 16] + __float_as_uint(nmu);
@@ -92,8 +92,12 @@ __global__ void __launch_bounds__(128, 2) rounds(unsigned long long* out, int it
       }
     }
     l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
-    NA_TMEM_ST32(trow + 128, sv);
-    NA_TMEM_ST32(trow + 160, (sv + 32));
+    if (NG == 4) {
+      NA_TMEM_ST32(trow + 128, sv);
+      NA_TMEM_ST32(trow + 160, (sv + 32));
+    } else {
+      NA_TMEM_ST32(trow + 64, sv);
+    }
     ptx::tmem_st_wait();
   }
   const unsigned long long t1 = clock64();
@@ -103,14 +107,14 @@ __global__ void __launch_bounds__(128, 2) rounds(unsigned long long* out, int it
   __syncthreads();
   if (warp == 0) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<256>(tmem);
+    ptx::tmem_dealloc<(NG == 4 ? 256 : 128)>(tmem);
   }
 }
 
 int main() {
   unsigned long long* d;
-  cudaMalloc(&d, 8 * 296);
-  unsigned long long h[296];
+  cudaMalloc(&d, 8 * 600);
+  unsigned long long h[600];
   auto run = [&](void (*k)(unsigned long long*, int, uint32_t), const char* name, int ctas, uint32_t wb) {
     k<<<ctas, 128>>>(d, 2000, wb);
     cudaMemcpy(h, d, 8 * ctas, cudaMemcpyDeviceToHost);
@@ -119,6 +123,7 @@ int main() {
     printf("%-28s ctas %d: %.0f clk per round per CTA (%s)\n", name, ctas, s / ctas,
            cudaGetErrorString(cudaGetLastError()));
   };
+  for (int per : {2, 3, 4}) run(rounds<0, 0, 2>, "64-col round", 148 * per, 0);
   for (int ctas : {148, 296}) {
     run(rounds<0, 0>, "full", ctas, 0);
     run(rounds<1, 0>, "full, partial mask", ctas, 0x00ffff00u);
