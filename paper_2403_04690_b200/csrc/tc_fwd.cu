@@ -280,9 +280,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       uint32_t mw[4];                             // this row's mask of the chunk
       r.chunk_mask(pl, org, mw);
       for (int j = 0; j < t.nchunks; ++j, ++kv) {
-        bool live[4];
+        // warp-uniform group flags before the wait (they depend on the mask only)
+        bool live[4], full[4];
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) live[gq] = __any_sync(0xffffffffu, mw[gq] != 0u);
+        for (int gq = 0; gq < 4; ++gq) {
+          live[gq] = __any_sync(0xffffffffu, mw[gq] != 0u);
+          full[gq] = __all_sync(0xffffffffu, mw[gq] == 0xffffffffu);
+        }
         ptx::mbar_wait(bar + B_S, kv & 1);
         ptx::tc_fence_after();
         if (tracer) NA_TRACE_EV(2, tr, 20);
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int gq = 0; gq < 4; ++gq) {
           if (!live[gq]) continue;
           const uint32_t w = mw[gq];
-          if (!__all_sync(0xffffffffu, w == 0xffffffffu)) {
+          if (!full[gq]) {
 #pragma unroll
             for (int c = 0; c < 32; ++c)
               sv[32 * gq + c] = (w >> c) & 1u ? sv[32 * gq + c] : __float_as_uint(-INFINITY);
