@@ -191,10 +191,14 @@ def test_baseline_config_sampled(na, name):
     torch.cuda.synchronize()
     BH, N, D = cfg.batch * cfg.heads, cfg.tokens, cfg.head_dim
     rng = np.random.default_rng(zlib.crc32(name.encode()))
-    n_f, n_b = (BH * N, BH * N) if name == "A" else (64, 12)
-    toks = np.sort(rng.choice(BH * N, size=n_f, replace=False))
-    # always include the first and last token of some slice (borders)
-    toks[0], toks[-1] = 0, BH * N - 1
+    n_f, n_b = (BH * N, BH * N) if name == "A" else (256, 48)
+    # the spatial corners and their neighbours (coordinates 0, 1, L-2, L-1 on
+    # every axis: clamped windows, ragged residue classes) of the first and
+    # the last (b, h) slice, plus uniformly drawn tokens
+    axes = [sorted({0, 1, e - 2, e - 1} & set(range(e))) for e in cfg.extent]
+    corners = [int(np.ravel_multi_index(c, cfg.extent)) for c in itertools.product(*axes)]
+    border = np.array([bh * N + c for bh in (0, BH - 1) for c in corners], dtype=np.int64)
+    toks = np.unique(np.concatenate([border, rng.choice(BH * N, size=n_f, replace=False)]))
     hq, hk, hv, hdo = (t.cpu() for t in (q, k, v, do))
     op = oracle_problem(cfg)
     ro, rlse = oracle.fwd_tokens(op, hq, hk, hv, toks)
@@ -202,7 +206,8 @@ def test_baseline_config_sampled(na, name):
     flat = lambda t: t.reshape(BH * N, -1)
     assert excess(flat(o)[toks].float().cpu(), ro, dt) <= 0
     assert max_err(lse.reshape(-1)[toks].cpu(), rlse) <= LSE_TOL[dt]
-    bt = toks if name == "A" else np.sort(rng.choice(BH * N, size=n_b, replace=False))
+    bt = toks if name == "A" else np.unique(np.concatenate(
+        [border[: len(corners)], rng.choice(BH * N, size=n_b, replace=False)]))
     rdq, rdk, rdv = oracle.bwd_tokens(op, hq, hk, hv, hdo, bt, stored_o=True)  # R12
     assert excess(flat(dq)[bt].float().cpu(), rdq, dt, grad_tol(dt)) <= 0
     assert excess(flat(dk)[bt].float().cpu(), rdk, dt, grad_tol(dt)) <= 0
