@@ -457,11 +457,7 @@ cudaError_t launch(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* 
   }
   const long long tiles = (long long)g.BH * pl.nres * pl.tiles;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-#ifdef NA_FWD_CTAS_PER_SM  // experiment knob (A/B builds only)
-  const long long per = NA_FWD_CTAS_PER_SM;
-#else
-  const long long per = 2;
-#endif
+  const long long per = 2;  // CTAs per SM (TMEM: 256 columns each)
   const unsigned grid = (unsigned)(tiles < per * num_sms() ? tiles : per * num_sms());
   prof_begin(KID_FWD_TC, st);
   kern<<<grid, kThreads, smem, st>>>(maps, g, pl, lse, (unsigned)tiles);

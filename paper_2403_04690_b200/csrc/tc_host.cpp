@@ -70,10 +70,9 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand)
     // softmax rounds per useful query row: chunks * (MMA columns + a fixed
     // per-round cost of kRoundCols columns).
     // The kTopPlans cheapest candidates are kept; `pick` selects one of them
-    // (0 = the model's choice; na_tune measures the others).
-    // NA_ROUND_COLS overrides the per-round cost (calibration experiments).
-    const char* env_cols = getenv("NA_ROUND_COLS");
-    const int kRoundCols = env_cols ? atoi(env_cols) : 96;
+    // (0 = the model's choice; na_tune measures the others).  The per-round
+    // cost (in MMA columns) was calibrated on the BASELINE configs.
+    constexpr int kRoundCols = 96;
     const int pick = std::min(std::max(pick_in, 0), kTopPlans - 1);
     const int R = g.rank;
     struct Cand {
