@@ -249,3 +249,49 @@ def test_every_candidate_plan_matches_oracle(na, ext, ker, dil, cau, D, dt):
         assert excess(dk.reshape(shp), rdk, dt, grad_tol(dt)) <= 0, pick
         assert excess(dv.reshape(shp), rdv, dt) <= 0, pick
     na.na_set_plan_choice(p, (0, 0, 0))
+
+
+# ------------------------------------------------------- randomized sweep
+
+def _random_cases(n=24, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        rank = int(rng.integers(1, 4))
+        ext, ker, dil, cau = [], [], [], []
+        for _ in range(rank):
+            L = int(rng.integers(3, {1: 700, 2: 48, 3: 18}[rank]))
+            c = int(rng.integers(0, 2))
+            d = int(rng.choice([1, 1, 2, 3]))
+            kmax = max(1, L // d)
+            k = int(rng.integers(1, min(kmax, {1: 160, 2: 11, 3: 7}[rank]) + 1))
+            if not c and k % 2 == 0:
+                k -= 1
+            if k < 1:
+                k = 1
+            ext.append(L), ker.append(k), dil.append(d), cau.append(c)
+        D = int(rng.choice([32, 64]))
+        dt = [torch.float16, torch.bfloat16][int(rng.integers(0, 2))]
+        out.append((ext, ker, dil, cau, D, dt))
+    return out
+
+
+@pytest.mark.parametrize("ext,ker,dil,cau,D,dt", _random_cases(64))
+def test_random_problems_match_oracle(na, ext, ker, dil, cau, D, dt):
+    """Seeded random shapes, windows, dilations, causal mixes, head dims and
+    dtypes on the tensor-core path (planner, masks, halos, ragged classes)."""
+    cfg = na_synth.small_config(ext, ker, dil, cau, head_dim=D, batch=1, heads=2, dtype=dt)
+    p = na.make_problem(1, 2, list(ext), D, ker, dil, [bool(c) for c in cau], dtype=dt, impl="tc")
+    if na.na_validate(p) != 0 or na.na_selected_impl(p) != na.NA_IMPL_TC:
+        pytest.skip("problem outside the tensor-core path")
+    q, k, v, do = na_synth.make_inputs(cfg, salt=17)
+    o, lse, dq, dk, dv = run_gpu(na, cfg, q, k, v, do, "tc")
+    op = oracle_problem(cfg)
+    ro, rlse = oracle.fwd(op, q, k, v)
+    rdq, rdk, rdv = oracle.bwd(op, q, k, v, do, stored_o=True)
+    shp = (1, 2, cfg.tokens, D)
+    assert excess(o.reshape(shp), ro, dt) <= 0
+    assert max_err(lse.reshape(shp[:-1]), rlse) <= LSE_TOL[dt]
+    assert excess(dq.reshape(shp), rdq, dt, grad_tol(dt)) <= 0
+    assert excess(dk.reshape(shp), rdk, dt, grad_tol(dt)) <= 0
+    assert excess(dv.reshape(shp), rdv, dt) <= 0
