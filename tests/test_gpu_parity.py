@@ -285,13 +285,17 @@ def test_random_problems_match_oracle(na, ext, ker, dil, cau, D, dt):
     if na.na_validate(p) != 0 or na.na_selected_impl(p) != na.NA_IMPL_TC:
         pytest.skip("problem outside the tensor-core path")
     q, k, v, do = na_synth.make_inputs(cfg, salt=17)
-    o, lse, dq, dk, dv = run_gpu(na, cfg, q, k, v, do, "tc")
     op = oracle_problem(cfg)
     ro, rlse = oracle.fwd(op, q, k, v)
     rdq, rdk, rdv = oracle.bwd(op, q, k, v, do, stored_o=True)
     shp = (1, 2, cfg.tokens, D)
-    assert excess(o.reshape(shp), ro, dt) <= 0
-    assert max_err(lse.reshape(shp[:-1]), rlse) <= LSE_TOL[dt]
-    assert excess(dq.reshape(shp), rdq, dt, grad_tol(dt)) <= 0
-    assert excess(dk.reshape(shp), rdk, dt, grad_tol(dt)) <= 0
-    assert excess(dv.reshape(shp), rdv, dt) <= 0
+    n = na.na_plan_candidates(p)
+    for pick in sorted({0, n - 1}):  # the model's plan and its last candidate
+        na.na_set_plan_choice(p, (pick, pick, pick))
+        o, lse, dq, dk, dv = run_gpu(na, cfg, q, k, v, do, "tc")
+        assert excess(o.reshape(shp), ro, dt) <= 0, pick
+        assert max_err(lse.reshape(shp[:-1]), rlse) <= LSE_TOL[dt], pick
+        assert excess(dq.reshape(shp), rdq, dt, grad_tol(dt)) <= 0, pick
+        assert excess(dk.reshape(shp), rdk, dt, grad_tol(dt)) <= 0, pick
+        assert excess(dv.reshape(shp), rdv, dt) <= 0, pick
+    na.na_set_plan_choice(p, (0, 0, 0))
