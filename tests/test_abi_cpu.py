@@ -122,3 +122,24 @@ def test_fwd_rejects_before_launch(na):
 def test_status_strings(na):
     for s in range(15):
         assert na.status_string(s)
+
+
+def test_plan_choice_host_api(na):
+    """Tile-plan tuning API (host side, no GPU): candidate counts, pick
+    round-trip, range checks."""
+    p1 = na.make_problem(1, 2, [300], 64, [7], dtype=torch.float16)
+    assert na.na_plan_candidates(p1) == 1            # rank 1: one plan
+    p32 = na.make_problem(1, 2, [16, 16], 16, [3, 3], dtype=torch.float32)
+    assert na.na_plan_candidates(p32) == 1           # SIMT path: nothing to tune
+    p3 = na.make_problem(1, 2, [16, 64, 64], 64, [7, 7, 7], is_causal=[True, False, False],
+                         dtype=torch.float16)
+    n = na.na_plan_candidates(p3)
+    assert 1 < n <= 4
+    assert na.na_get_plan_choice(p3) == (0, 0, 0)    # the model's plan by default
+    na.na_set_plan_choice(p3, (n - 1, 0, 1))
+    assert na.na_get_plan_choice(p3) == (n - 1, 0, 1)
+    with pytest.raises(na.NAError):
+        na.na_set_plan_choice(p3, (n, 0, 0))
+    na.na_set_plan_choice(p3, (0, 0, 0))
+    bad = na.make_problem(1, 2, [8], 64, [9], dtype=torch.float16)  # window exceeds extent
+    assert na.na_plan_candidates(bad) == -1
