@@ -66,7 +66,8 @@ def algorithmic_bytes(cfg, kernel):
         "fna_bwd_pre": 2 * E * s + 12 * rows,          # O, dO, LSE read; (-LSE log2 e, D) written
         "fna_dkdv_tc": 6 * E * s + 8 * rows,           # Q,K,V,dO read; dK,dV write; LSE,D read
         "fna_dkdv_simt": 6 * E * s + 8 * rows,
-        "fna_dq_tc": 5 * E * s + 8 * rows,             # Q,K,V,dO read; dQ write; LSE,D read
+        # Rank 1 fuses the preprocess into dQ: + O read, LSE read, (-LSE log2 e, D) written.
+        "fna_dq_tc": (6 * E * s + 12 * rows) if len(cfg.extent) == 1 else (5 * E * s + 8 * rows),
         "fna_dq_simt": 5 * E * s + 8 * rows,
     }[kernel]
 

@@ -420,6 +420,13 @@ cudaError_t simt_fwd(int dtype, const Geom& g, const void* q, const void* k, con
   }
 }
 
+cudaError_t rv_clear_padding(const Geom& g, float* Dvec, cudaStream_t st) {
+  bool ragged = g.rv_lc[g.rank - 1] * g.dil[g.rank - 1] != g.L[g.rank - 1];
+  for (int a = 0; a + 1 < g.rank; ++a) ragged = ragged || g.L[a] % g.dil[a] != 0;
+  if (!ragged) return cudaSuccess;
+  return cudaMemsetAsync(Dvec, 0, (size_t)g.BH * g.nres * 2 * g.rv_plane * sizeof(float), st);
+}
+
 cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, const float* lse,
                            float* Dvec, cudaStream_t st) {
   const int64_t rows = (int64_t)g.BH * g.N;

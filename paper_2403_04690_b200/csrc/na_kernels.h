@@ -32,6 +32,9 @@ cudaError_t simt_bwd(int dtype, const Geom& g, const void* q, const void* k, con
 // D_x = <dO_x, O_x> (fp32).  lse == nullptr: D_x at the token index of Dvec
 // [BH*N].  lse != nullptr (16-bit only): the tensor-core row-vector layout
 // (-LSE_x*log2(e), D_x) of Geom::rv_* in Dvec.
+// Zero the row-vector layout's padding slots (ragged residue classes) before
+// the tensor-core backward writes the rest.
+cudaError_t rv_clear_padding(const Geom& g, float* Dvec, cudaStream_t st);
 cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, const float* lse,
                            float* Dvec, cudaStream_t st);
 

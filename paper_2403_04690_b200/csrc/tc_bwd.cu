@@ -58,15 +58,20 @@ constexpr int kMmaWarp = 9;    // TMEM owner; OUT MMAs (dV, dK | dQ), in sub-chu
 constexpr int kSWarp = 10;     // S / dP MMAs, as far ahead as the TMEM buffers allow
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <int D>
+// Both kernels stream 4 stages; a fused dQ (FUSE: rank 1) holds the O tiles
+// it reads to form the row vectors itself (see the dQ compute warps) where
+// dK/dV keeps the gathered row vectors of its streamed chunks.
+template <int D, bool KV, bool FUSE>
 struct BwdSmem {
+  static constexpr int kSt = 4;                       // streamed stages
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTile = 128 * kRowBytes;
   static constexpr int kA = 0;                        // stationary [2 bufs][2 tiles] (K,V | Q,dO)
-  static constexpr int kB0 = kA + 4 * kTile;          // streamed [kStages] (Q | K)
-  static constexpr int kB1 = kB0 + kStages * kTile;   // streamed [kStages] (dO | V)
-  static constexpr int kVec = kB1 + kStages * kTile;  // [kStages][-LSE2 x128 | D x128] fp32 (dK/dV)
-  static constexpr int kBar = kVec + kStages * 256 * 4;
+  static constexpr int kO = kA + 4 * kTile;           // fused dQ: stationary O tile [2 bufs]
+  static constexpr int kB0 = kO + (FUSE ? 2 * kTile : 0);  // streamed [kSt] (Q | K)
+  static constexpr int kB1 = kB0 + kSt * kTile;       // streamed [kSt] (dO | V)
+  static constexpr int kVec = kB1 + kSt * kTile;      // [kSt][-LSE2 x128 | D x128] fp32 (dK/dV)
+  static constexpr int kBar = kVec + (KV ? kSt * 256 * 4 : 0);
   static constexpr int kBytes = kBar + 256;
 };
 
@@ -97,18 +102,25 @@ enum : int {
 // chunks b0, b1; output tiles out0 (, out1) stored with TMA (stationary box).
 struct BwdMaps {
   CUtensorMap a0, a1, b0, b1, out0, out1;
+  CUtensorMap o;  // dQ: the stationary tile's O rows (fused preprocess)
 };
 
 template <int RANK, int D, bool BF16, bool KV_STATIONARY>
 __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, const TcPlan& pl,
-                                         const float* __restrict__ rv, unsigned num_tiles) {
+                                         float* __restrict__ rv, const float* __restrict__ lse,
+                                         unsigned num_tiles) {
   const CUtensorMap& map_a0 = maps.a0;
   const CUtensorMap& map_a1 = maps.a1;
   const CUtensorMap& map_b0 = maps.b0;
   const CUtensorMap& map_b1 = maps.b1;
   const CUtensorMap& map_out0 = maps.out0;
   const CUtensorMap& map_out1 = maps.out1;
-  using S = BwdSmem<D>;
+  // dQ forms the row vectors itself (fused preprocess) for rank 1; for
+  // multi-dimensional tiles the extra per-tile work measured slower than the
+  // separate preprocess pass, so there dQ reads them.
+  constexpr bool kFuse = !KV_STATIONARY && RANK == 1;
+  using S = BwdSmem<D, KV_STATIONARY, kFuse>;
+  constexpr int kStages = S::kSt;
   // Output accumulator columns per tile; double-buffered when two fit.
   constexpr int kOutCols = KV_STATIONARY ? 2 * D : D;
   constexpr bool kOutDouble = 2 * kOutCols <= 128;
@@ -141,7 +153,9 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     }
     ptx::fence_barrier_init();
   }
-  for (int i = threadIdx.x; i < kStages * 256; i += kThreads) vec[i] = 0.f;  // unloaded columns read 0
+  if constexpr (KV_STATIONARY) {  // (dQ has no row-vector stages)
+    for (int i = threadIdx.x; i < kStages * 256; i += kThreads) vec[i] = 0.f;  // unloaded columns read 0
+  }
   ptx::fence_proxy_async();  // before TMA writes the same smem
   if (pl.rows_kv < 128) {  // rows no TMA box writes must be finite (zero)
     const int nz = (128 - pl.rows_kv) * S::kRowBytes / 16;
@@ -180,12 +194,15 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       if (NA_BWD_TRACE_ON) NA_TRACE_EV(0, tr, 1);
       uint8_t* a0 = smem + S::kA + (2 * ab) * S::kTile;
       uint8_t* a1 = a0 + S::kTile;
-      ptx::mbar_expect_tx_w(bar + B_AF + ab, 2 * 128 * S::kRowBytes);
+      ptx::mbar_expect_tx_w(bar + B_AF + ab, (kFuse ? 3 : 2) * 128 * S::kRowBytes);
       for (int i = 0; i < pl.q_issues; ++i) {
         t.template load_box<RANK>(&map_a0, a0 + i * pl.q_box_x * S::kRowBytes, bar + B_AF + ab,
                                   t.q_origin, i * pl.q_box_x, g);
         t.template load_box<RANK>(&map_a1, a1 + i * pl.q_box_x * S::kRowBytes, bar + B_AF + ab,
                                   t.q_origin, i * pl.q_box_x, g);
+        if constexpr (kFuse)
+          t.template load_box<RANK>(&maps.o, smem + S::kO + ab * S::kTile + i * pl.q_box_x * S::kRowBytes,
+                                    bar + B_AF + ab, t.q_origin, i * pl.q_box_x, g);
       }
       for (int j = 0; j < t.nchunks; ++j, ++kv_it) {
         const int s = kv_it % kStages;
@@ -358,9 +375,17 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     int tr = 0;
     (void)tr;
     const bool tracer = NA_BWD_TRACE_ON && lane == 0 && (warp == 0 || warp == 4);
-    // Row (query) values (-LSE * log2(e), D) of a Q-stationary tile, from the
-    // row-vector layout written by the preprocess kernel.
-    auto row_vals = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r, float& nl2, float& d) {
+    // A Q-stationary tile's row values (-LSE*log2(e), D = <dO, O>).
+    // Fused preprocess (kFuse): -LSE*log2(e) from the LSE (prefetched from
+    // global) and D from the stationary dO tile and the O tile loaded with
+    // it, kept in registers for this kernel and written to the row-vector
+    // layout (warpgroup 0) for the dK/dV kernel, which runs next; replaces
+    // the separate preprocess pass over O and dO.  Otherwise: read from the
+    // row-vector layout the preprocess kernel wrote.
+    auto row_lse = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r) {
+      return r.valid ? lse[r.out_offset(g, t) / g.D] : 0.f;
+    };
+    auto row_read = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r, float& nl2, float& d) {
       nl2 = 0.f;
       d = 0.f;
       if (r.valid) {
@@ -369,6 +394,35 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         for (int a = 0; a < RANK; ++a) i += (long long)r.c[a] * g.rv_cs[a];
         nl2 = rv[i];
         d = rv[i + g.rv_plane];
+      }
+    };
+    auto row_vals = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r, uint32_t tix, float lse_v,
+                        float& nl2, float& d) {
+      const int ab = tix & 1;
+      ptx::mbar_wait(bar + B_AF + ab, (tix >> 1) & 1);
+      const uint8_t* ot = smem + S::kO + ab * S::kTile;
+      const uint8_t* dt = smem + S::kA + (2 * ab + 1) * S::kTile;
+      float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+      for (int c = 0; c < D / 8; ++c) {
+        const uint4 a = *reinterpret_cast<const uint4*>(ot + ptx::swz_off(row, c, S::kRowBytes));
+        const uint4 b = *reinterpret_cast<const uint4*>(dt + ptx::swz_off(row, c, S::kRowBytes));
+        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 fa = unpack2<BF16>(aw[e]), fb = unpack2<BF16>(bw[e]);
+          acc0 = fmaf(fa.x, fb.x, acc0);
+          acc1 = fmaf(fa.y, fb.y, acc1);
+        }
+      }
+      nl2 = r.valid ? -lse_v * kLog2e : 0.f;
+      d = r.valid ? acc0 + acc1 : 0.f;
+      if (grp == 0 && r.valid) {
+        long long i = rv_base(g, t.bh, t.res);
+#pragma unroll
+        for (int a = 0; a < RANK; ++a) i += (long long)r.c[a] * g.rv_cs[a];
+        rv[i] = nl2;
+        rv[i + g.rv_plane] = d;
       }
     };
     // ---- epilogue of a finished tile ----
@@ -449,8 +503,10 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     unsigned tile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, t);
     if (tile < num_tiles) r.init(g, pl, t, row, /*inverse=*/KV_STATIONARY);
     float row_nl2 = 0.f, row_d = 0.f;
-    if constexpr (!KV_STATIONARY) {
-      if (tile < num_tiles) row_vals(t, r, row_nl2, row_d);
+    if constexpr (kFuse) {
+      if (tile < num_tiles) row_vals(t, r, 0, row_lse(t, r), row_nl2, row_d);
+    } else if constexpr (!KV_STATIONARY) {
+      if (tile < num_tiles) row_read(t, r, row_nl2, row_d);
     }
     uint32_t kv_base = 0;
     while (tile < num_tiles) {
@@ -467,7 +523,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       RowCtx<RANK> rn;
       unsigned tile_n = num_tiles;
       bool tn_known = false;
-      float nrow_nl2 = 0.f, nrow_d = 0.f;
+      float nrow_nl2 = 0.f, nrow_d = 0.f;  // (kFuse: nrow_nl2 holds the prefetched LSE)
       // This group's sub-chunks u_first, u_first + 2, ...: chunk origins by
       // odometer (one chunk per step when a chunk has two sub-chunks, two
       // otherwise); each mask is computed in the previous sub-chunk's load shadow.
@@ -489,7 +545,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           tn_known = true;
           if (tile_n < num_tiles) {
             rn.init(g, pl, tn, row, /*inverse=*/KV_STATIONARY);
-            if constexpr (!KV_STATIONARY) row_vals(tn, rn, nrow_nl2, nrow_d);
+            if constexpr (kFuse) nrow_nl2 = row_lse(tn, rn);  // LSE prefetch
+            else if constexpr (!KV_STATIONARY) row_read(tn, rn, nrow_nl2, nrow_d);
           }
         }
         const uint32_t b3 = gu % 3;
@@ -601,14 +658,19 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         tile_n = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, tn);
         if (tile_n < num_tiles) {
           rn.init(g, pl, tn, row, /*inverse=*/KV_STATIONARY);
-          if constexpr (!KV_STATIONARY) row_vals(tn, rn, nrow_nl2, nrow_d);
+          if constexpr (kFuse) nrow_nl2 = row_lse(tn, rn);
+          else if constexpr (!KV_STATIONARY) row_read(tn, rn, nrow_nl2, nrow_d);
         }
       }
       tile = tile_n;
       t = tn;
       r = rn;
-      row_nl2 = nrow_nl2;
-      row_d = nrow_d;
+      if constexpr (kFuse) {
+        if (tile < num_tiles) row_vals(t, r, ti, nrow_nl2, row_nl2, row_d);
+      } else {
+        row_nl2 = nrow_nl2;
+        row_d = nrow_d;
+      }
       if (tracer) NA_TRACE_EV(2 + grp, tr, 23);
     }
     if (pend) {
@@ -634,30 +696,32 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
 // dK, dV: key-stationary over the inverse halo.
 template <int RANK, int D, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    fna_dkdv_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, const float* __restrict__ rv,
+    fna_dkdv_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, float* __restrict__ rv,
                 unsigned num_tiles) {
-  bwd_body<RANK, D, BF16, true>(maps, g, pl, rv, num_tiles);
+  bwd_body<RANK, D, BF16, true>(maps, g, pl, rv, nullptr, num_tiles);
 }
 
 // dQ: query-stationary over the forward halo.
 template <int RANK, int D, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    fna_dq_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, const float* __restrict__ rv,
-              unsigned num_tiles) {
-  bwd_body<RANK, D, BF16, false>(maps, g, pl, rv, num_tiles);
+    fna_dq_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, float* __restrict__ rv,
+              const float* __restrict__ lse, unsigned num_tiles) {
+  bwd_body<RANK, D, BF16, false>(maps, g, pl, rv, lse, num_tiles);
 }
 
 template <int RANK, int D, bool BF16>
 cudaError_t launch_both(const Geom& g, const TcPlan* pls, const BwdMaps& mkv, const BwdMaps& mq,
-                        const float* rv, cudaStream_t st) {
-  const int smem = BwdSmem<D>::kBytes + 1024;
+                        float* rv, const float* lse, cudaStream_t st) {
+  constexpr bool kFuse = RANK == 1;  // dQ forms the row vectors (see bwd_body)
+  const int smem_kv = BwdSmem<D, true, false>::kBytes + 1024;
+  const int smem_q = BwdSmem<D, false, kFuse>::kBytes + 1024;
   auto kdkdv = fna_dkdv_tc<RANK, D, BF16>;
   auto kdq = fna_dq_tc<RANK, D, BF16>;
-  static bool attr = false;
+  static bool attr = false;  // benign race: idempotent
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kdkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(kdkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kdq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = cudaFuncSetAttribute(kdq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -666,26 +730,28 @@ cudaError_t launch_both(const Geom& g, const TcPlan* pls, const BwdMaps& mkv, co
   if (tiles_kv > 0x7fffffffLL || tiles_q > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const unsigned grid_kv = (unsigned)(tiles_kv < num_sms() ? tiles_kv : num_sms());
   const unsigned grid_q = (unsigned)(tiles_q < num_sms() ? tiles_q : num_sms());
-  prof_begin(KID_DKDV_TC, st);
-  kdkdv<<<grid_kv, kThreads, smem, st>>>(mkv, g, pls[0], rv, (unsigned)tiles_kv);
+  // dQ first: when fused it also writes the row vectors (-LSE*log2(e), D)
+  // the dK/dV kernel streams.
+  prof_begin(KID_DQ_TC, st);
+  kdq<<<grid_q, kThreads, smem_q, st>>>(mq, g, pls[1], rv, lse, (unsigned)tiles_q);
   prof_end(st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  prof_begin(KID_DQ_TC, st);
-  kdq<<<grid_q, kThreads, smem, st>>>(mq, g, pls[1], rv, (unsigned)tiles_q);
+  prof_begin(KID_DKDV_TC, st);
+  kdkdv<<<grid_kv, kThreads, smem_kv, st>>>(mkv, g, pls[0], rv, (unsigned)tiles_kv);
   prof_end(st);
   return cudaGetLastError();
 }
 
 template <int RANK>
 cudaError_t by_type(int dtype, const Geom& g, const TcPlan* pl, const BwdMaps& mkv, const BwdMaps& mq,
-                    const float* rv, cudaStream_t st) {
+                    float* rv, const float* lse, cudaStream_t st) {
   const bool bf = dtype == 2;
   if (g.D == 64)
-    return bf ? launch_both<RANK, 64, true>(g, pl, mkv, mq, rv, st)
-              : launch_both<RANK, 64, false>(g, pl, mkv, mq, rv, st);
-  return bf ? launch_both<RANK, 32, true>(g, pl, mkv, mq, rv, st)
-            : launch_both<RANK, 32, false>(g, pl, mkv, mq, rv, st);
+    return bf ? launch_both<RANK, 64, true>(g, pl, mkv, mq, rv, lse, st)
+              : launch_both<RANK, 64, false>(g, pl, mkv, mq, rv, lse, st);
+  return bf ? launch_both<RANK, 32, true>(g, pl, mkv, mq, rv, lse, st)
+            : launch_both<RANK, 32, false>(g, pl, mkv, mq, rv, lse, st);
 }
 
 }  // namespace
@@ -695,7 +761,10 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
                    float* Dvec, cudaStream_t st, int* launches) {
   const char* why;
   if (!tc_supported(dtype, g, &why)) return cudaErrorNotSupported;
-  cudaError_t e = bwd_preprocess(dtype, g, o, d_o, lse, Dvec, st);  // row-vector layout
+  // Row-vector layout: rank 1, written by the dQ kernel (fused preprocess;
+  // slots no token maps to, ragged residue classes, must read as 0);
+  // otherwise by the preprocess kernel.
+  cudaError_t e = g.rank == 1 ? rv_clear_padding(g, Dvec, st) : bwd_preprocess(dtype, g, o, d_o, lse, Dvec, st);
   if (e != cudaSuccess) return e;
   // Each kernel has its own plan (na_tune may measure different winners).
   const PlanChoice pc = plan_choice(g, dtype);
@@ -717,11 +786,13 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   if ((e = make_map(&mkv.out1, dtype, g, dv, pls[0].tq, pls[0].q_box_x)) != cudaSuccess) return e;
   if ((e = make_map(&mq.out0, dtype, g, dq, pls[1].tq, pls[1].q_box_x)) != cudaSuccess) return e;
   mq.out1 = mq.out0;
-  *launches = 3;
+  if ((e = make_map(&mq.o, dtype, g, o, pls[1].tq, pls[1].q_box_x)) != cudaSuccess) return e;
+  mkv.o = mq.o;
+  *launches = g.rank == 1 ? 2 : 3;
   switch (g.rank) {
-    case 1: return by_type<1>(dtype, g, pls, mkv, mq, Dvec, st);
-    case 2: return by_type<2>(dtype, g, pls, mkv, mq, Dvec, st);
-    default: return by_type<3>(dtype, g, pls, mkv, mq, Dvec, st);
+    case 1: return by_type<1>(dtype, g, pls, mkv, mq, Dvec, lse, st);
+    case 2: return by_type<2>(dtype, g, pls, mkv, mq, Dvec, lse, st);
+    default: return by_type<3>(dtype, g, pls, mkv, mq, Dvec, lse, st);
   }
 }
 

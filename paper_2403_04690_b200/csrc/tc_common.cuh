@@ -33,6 +33,15 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   }
 }
 
+template <bool BF16>
+__device__ __forceinline__ float2 unpack2(uint32_t w) {
+  if constexpr (BF16) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+  } else {
+    return __half22float2(*reinterpret_cast<const __half2*>(&w));
+  }
+}
+
 // 2^x for a pair of values on the FMA pipe (the MUFU ex2 unit is the
 // scarcest resource of the softmax): Cody-Waite split x = n + f with
 // n = rint(x), f in [-0.5, 0.5]; 2^f by a degree-3 polynomial with c0 = 1
