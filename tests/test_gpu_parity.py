@@ -129,18 +129,21 @@ def test_small_sweep_matches_oracle(na, impl, ext, ker, dil, cau, D, dt):
 
 @pytest.mark.parametrize("impl", ["simt", "tc"])
 @pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
-def test_kernel_one_is_exact(na, impl, dt):
+@pytest.mark.parametrize("ext,dil", [([9, 20], [1, 2]), ([301], [3])])
+def test_kernel_one_is_exact(na, impl, dt, ext, dil):
     """kernel size 1 -> O == V bitwise, dV == dO bitwise, dQ = dK = 0.
     dQ/dK are P (dP - D) with P = 1: zero up to the rounding difference of two
-    fp32 dot products summed in different orders (D_x by the preprocess
-    kernel, dP by the tensor core), hence |dQ|, |dK| <= 1e-5."""
-    cfg = na_synth.small_config([9, 20], [1, 1], [1, 2], [0, 0], head_dim=64, dtype=dt)
-    p = na.make_problem(1, 2, [9, 20], 64, [1, 1], [1, 2], dtype=dt, impl=impl)
+    fp32 dot products summed in different orders (D_x by the preprocess --
+    for 1-D inside the dQ kernel -- dP by the tensor core), hence
+    |dQ|, |dK| <= 1e-5."""
+    ker = [1] * len(ext)
+    cfg = na_synth.small_config(ext, ker, dil, [0] * len(ext), head_dim=64, dtype=dt)
+    p = na.make_problem(1, 2, ext, 64, ker, dil, dtype=dt, impl=impl)
     if impl == "tc" and na.na_selected_impl(p) != na.NA_IMPL_TC:
         pytest.skip("problem outside the tensor-core path")
     q, k, v, do = na_synth.make_inputs(cfg, device="cuda", salt=3)
-    o, lse = na.na_fwd(q, k, v, [1, 1], [1, 2], impl=impl)
-    dq, dk, dv = na.na_bwd(q, k, v, o, do, lse, [1, 1], [1, 2], impl=impl)
+    o, lse = na.na_fwd(q, k, v, ker, dil, impl=impl)
+    dq, dk, dv = na.na_bwd(q, k, v, o, do, lse, ker, dil, impl=impl)
     assert torch.equal(o, v)
     assert torch.equal(dv, do)
     assert dq.abs().max() <= 1e-5 and dk.abs().max() <= 1e-5
@@ -159,6 +162,29 @@ def test_no_nan_with_masked_chunks(na, impl):
     dq, dk, dv = na.na_bwd(q, k, v, o, do, lse, **kw)
     for t in (o, lse, dq, dk, dv):
         assert torch.isfinite(t).all()
+
+
+@pytest.mark.parametrize("ext,ker,dil,kernels", [
+    ([1000], [33], [3], ["fna_dq_tc", "fna_dkdv_tc"]),  # 1-D: preprocess fused into dQ
+    ([40, 24], [7, 7], [2, 1], ["fna_bwd_pre", "fna_dq_tc", "fna_dkdv_tc"]),
+])
+def test_backward_launch_structure(na, ext, ker, dil, kernels):
+    """The tensor-core backward launches exactly the kernels DESIGN.md
+    section 1 lists (B1-B3), in order, and reports that count."""
+    cfg = na_synth.small_config(ext, ker, dil, [0] * len(ext), head_dim=64, dtype=torch.float16)
+    q, k, v, do = (t.cuda() for t in na_synth.make_inputs(cfg, salt=2))
+    o, lse = na.na_fwd(q, k, v, ker, dil, impl="tc")
+    torch.cuda.synchronize()
+    na.profile_enable(True)
+    try:
+        na.na_bwd(q, k, v, o, do, lse, ker, dil, impl="tc")
+        n = na.last_launch_count()
+        rec = na.profile_collect()
+    finally:
+        na.profile_enable(False)
+    names = [r[0].split("<")[0] for r in rec]
+    assert names == kernels, names
+    assert n == len(kernels)
 
 
 def test_deterministic(na):
