@@ -187,6 +187,36 @@ def test_backward_launch_structure(na, ext, ker, dil, kernels):
     assert n == len(kernels)
 
 
+@pytest.mark.parametrize("ext,ker,dil,cau", [([1000], [33], [3], [1]), ([8, 9, 12], [3, 3, 3], [2, 1, 2], [0, 1, 0])])
+def test_cuda_graph_capture(na, ext, ker, dil, cau):
+    """na_fwd + na_bwd captured in a CUDA graph (launch-bound
+    small shards) replay to the eager results bit for bit: the ABI issues
+    only stream-ordered work on the caller's stream."""
+    cfg = na_synth.small_config(ext, ker, dil, cau, head_dim=64, dtype=torch.bfloat16)
+    q, k, v, do = (t.cuda() for t in na_synth.make_inputs(cfg, salt=9))
+    kw = dict(kernel_size=ker, dilation=dil, is_causal=[bool(c) for c in cau], impl="tc")
+
+    def step():
+        o, lse = na.na_fwd(q, k, v, **kw)
+        return (o, lse) + tuple(na.na_bwd(q, k, v, o, do, lse, **kw))
+
+    ref = [t.clone() for t in step()]
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        outs = step()
+    for t in outs:
+        t.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
+
+
 def test_deterministic(na):
     cfg = na_synth.small_config([40, 24], [7, 7], [2, 1], [0, 1], head_dim=64, dtype=torch.bfloat16)
     q, k, v, do = (t.cuda() for t in na_synth.make_inputs(cfg, salt=5))
