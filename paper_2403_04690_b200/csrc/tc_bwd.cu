@@ -402,21 +402,18 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       ptx::mbar_wait(bar + B_AF + ab, (tix >> 1) & 1);
       const uint8_t* ot = smem + S::kO + ab * S::kTile;
       const uint8_t* dt = smem + S::kA + (2 * ab + 1) * S::kTile;
-      float acc0 = 0.f, acc1 = 0.f;
+      float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // two packed-FMA chains
 #pragma unroll
       for (int c = 0; c < D / 8; ++c) {
         const uint4 a = *reinterpret_cast<const uint4*>(ot + ptx::swz_off(row, c, S::kRowBytes));
         const uint4 b = *reinterpret_cast<const uint4*>(dt + ptx::swz_off(row, c, S::kRowBytes));
         const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 fa = unpack2<BF16>(aw[e]), fb = unpack2<BF16>(bw[e]);
-          acc0 = fmaf(fa.x, fb.x, acc0);
-          acc1 = fmaf(fa.y, fb.y, acc1);
-        }
+        for (int e = 0; e < 4; ++e)
+          acc[e & 1] = __ffma2_rn(unpack2<BF16>(aw[e]), unpack2<BF16>(bw[e]), acc[e & 1]);
       }
       nl2 = r.valid ? -lse_v * kLog2e : 0.f;
-      d = r.valid ? acc0 + acc1 : 0.f;
+      d = r.valid ? (acc[0].x + acc[1].x) + (acc[0].y + acc[1].y) : 0.f;
       if (grp == 0 && r.valid) {
         long long i = rv_base(g, t.bh, t.res);
 #pragma unroll
