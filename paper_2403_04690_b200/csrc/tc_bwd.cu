@@ -152,6 +152,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       ptx::mbar_init(bar + B_E + s, 1);
     }
     ptx::fence_barrier_init();
+    tmem_slot[1] = tmem_slot[2] = 0u;  // dQ drain counters
   }
   if constexpr (KV_STATIONARY) {  // (dQ has no row-vector stages)
     for (int i = threadIdx.x; i < kStages * 256; i += kThreads) vec[i] = 0.f;  // unloaded columns read 0
@@ -369,8 +370,13 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     const int gtid = (warp & 3) * 32 + lane;  // 0..127 within the group
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = g.scale_log2;
-    // TMA-store issuer: dK/dV, thread 0 of the draining group; dQ, thread 0.
-    const bool issuer = KV_STATIONARY ? (gtid == 0) : (threadIdx.x == 0);
+    // TMA-store issuer: dK/dV, thread 0 of the draining group; dQ, thread 0
+    // of whichever group finishes its half of the drain second (rank 1, 2;
+    // for rank 3 that measured slower -- E dQ 1.51 -> 1.59 ms -- and there
+    // both groups meet at a barrier and thread 0 stores).
+    constexpr bool kLateStore = !KV_STATIONARY && RANK < 3;
+    const bool issuer = (KV_STATIONARY || kLateStore) ? (gtid == 0) : (threadIdx.x == 0);
+    uint32_t* drain_cnt = tmem_slot + 1;  // dQ: halves drained per output buffer [2] (monotone)
     uint32_t ub = 0, ti = 0;
     int tr = 0;
     (void)tr;
@@ -480,9 +486,20 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       ptx::mbar_arrive(bar + B_OE + ob);
       ptx::fence_proxy_async();  // staged tile visible to the TMA engine
       if (tracer) NA_TRACE_EV(2 + grp, tr, 25);
-      if constexpr (KV_STATIONARY) ptx::named_bar_sync(3 + grp, 128);
+      if constexpr (KV_STATIONARY || kLateStore) ptx::named_bar_sync(3 + grp, 128);
       else ptx::named_bar_sync(3, kCompute);
-      if (issuer) {
+      bool store_now = issuer;
+      if constexpr (kLateStore) {
+        // The two groups drain at different times (a sub-chunk apart):
+        // the later one stores, so neither waits for the other.
+        if (issuer) {
+          uint32_t old;
+          asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                       : "=r"(old) : "r"(ptx::smem_u32(drain_cnt + ob)) : "memory");
+          store_now = (old & 1u) == 1u;
+        }
+      }
+      if (store_now) {
         for (int i = 0; i < pl.q_issues; ++i) {
           t.template store_box<RANK>(&map_out0, stage0 + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
           if constexpr (KV_STATIONARY)
