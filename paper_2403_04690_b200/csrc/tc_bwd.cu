@@ -449,7 +449,24 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       }
     };
     auto drain = [&](uint32_t src, uint8_t* stage, int col0, int ncols, float mul) {
-      for (int c0 = 0; c0 < ncols; c0 += 16) {
+      // 32 columns per TMEM round trip (two loads, one wait): the drain is
+      // latency-bound on tcgen05.ld -> wait.
+      int c0 = 0;
+      for (; c0 + 32 <= ncols; c0 += 32) {
+        uint32_t ov[32];
+        NA_TMEM_LD32(trow + src + c0, ov);
+        ptx::tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2)
+          pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
+        const int chunk = (col0 + c0) / 8;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + q, S::kRowBytes)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
+      if (c0 < ncols) {  // a 16-column remainder (dQ halves at D = 32)
         uint32_t ov[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
