@@ -14,7 +14,11 @@
 //                dS^T = P^T (dP^T - D_q) by the compute warps (written back to
 //                TMEM as 16-bit), then dV += P^T dO and dK += dS^T Q (TS MMAs).
 //   fna_dq_tc    query-stationary over the forward halo: S = Q K^T, dP = dO V^T,
-//                dS = P (dP - D), dQ += dS K.
+//                dS = P (dP - D), dQ += dS K.  For 1-D it also forms the
+//                row vectors (-LSE log2 e, D) itself from an O tile loaded
+//                with the stationary Q/dO tiles, and writes them for
+//                fna_dkdv_tc, which runs after it (the fused preprocess);
+//                2-D/3-D read them from the preprocess kernel.
 // Persistent, 1 CTA per SM walking tiles blockIdx.x, +gridDim.x, ...
 // Warp roles (352 threads): warps 0..7 two compute warpgroups (thread = TMEM
 // lane = stationary row); warp 8 TMA producer (stationary tiles double-
@@ -26,7 +30,9 @@
 //   issues the accumulating MMAs in order; their completion (B_PE) frees the
 //   buffer for S/dP(gu+3).  No warpgroup ever waits for an OUT MMA.
 // dK|dV share one 128-column accumulator drained at each tile start by the
-// warpgroup not owning the tile's first sub-chunk; dQ's is double-buffered.
+// warpgroup not owning the tile's first sub-chunk; dQ's is double-buffered,
+// each warpgroup drains half after its first sub-chunk of the next tile, and
+// the one finishing second issues the store (ranks 1, 2).
 // Outputs are staged in the tile's dead stationary smem and TMA-stored.
 #include <cuda.h>
 #include <cuda_bf16.h>
