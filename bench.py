@@ -12,13 +12,20 @@ batch (every §8(a) row of SURVEY.md).  Inputs are unit-normal, seeded per
 metric/unit: BASELINE.json's metric; `value` = effective TFLOP/s of the whole
 step over all ranks, with the paper's nominal FLOP count 4*N*l*D per (b,h)
 forward (P:369) and 10*N*l*D backward (2.5x, FlashAttention convention);
-l = 255.  Multi-GPU (torchrun): each rank owns its own contiguous range of
-B*H slices (weak scaling, no collective on the data path); NCCL only gathers
-timings.  Device time = CUDA events on the launch stream, max over ranks.
+l = 255.  Multi-GPU (torchrun): the config's B*H slices are
+split across the ranks -- rank g owns the flattened slices
+[g*BH/G, (g+1)*BH/G), seeded by global slice index -- so every N computes
+exactly BASELINE.json's problem (strong scaling, no collective on the data
+path); NCCL only gathers timings and parity errors.  Device time = CUDA
+events on the launch stream, max over ranks.
 
-`per_config` in the JSON line: fwd ms and fwd+bwd ms of EVERY BASELINE.json
-config (B's four variants, C at dilation 1 and 8, D, E), with effective
-TFLOP/s and the fractions of the tensor peak and (forward) of HBM bandwidth.
+`per_config` in the JSON line: every BASELINE.json config (A; B's four
+variants; C at dilation 1 and 8; D; E): fwd ms and fwd+bwd ms, effective
+TFLOP/s, the fractions of the tensor peak and (forward) of HBM bandwidth,
+the max-abs errors of O, LSE, dQ, dK, dV on the first and the last (b,h)
+slice (every token) against the fp64 oracle's exact result (and, on the
+first slice, dQ/dK against the oracle's stored-O reading R12), and the
+oracle's own time on those slices extrapolated to the whole config.
 
 `--impl reference`: the arm the driver compares against is the fp64 CPU
 oracle (oracle/, test infrastructure) timed on this host's cores on a
@@ -54,11 +61,13 @@ def flops(cfg, fwd=True, bwd=True):
     return (per if fwd else 0.0) + (2.5 * per if bwd else 0.0)
 
 
-def algorithmic_bytes(cfg, kernel):
+def algorithmic_bytes(cfg, kernel, bh=None):
     """Bytes a kernel must move at minimum: every
-    tensor it reads or writes once.  E = elements of one [B,H,N,D] tensor."""
-    E = cfg.batch * cfg.heads * cfg.tokens * cfg.head_dim
-    rows = cfg.batch * cfg.heads * cfg.tokens
+    tensor it reads or writes once, for `bh` (b,h) slices (default: the whole
+    config).  E = elements of one [B,H,N,D] tensor."""
+    bh = cfg.batch * cfg.heads if bh is None else bh
+    E = bh * cfg.tokens * cfg.head_dim
+    rows = bh * cfg.tokens
     s = 2 if cfg.dtype in (torch.float16, torch.bfloat16) else 4
     return {
         "fna_fwd_tc": 4 * E * s + 4 * rows,            # Q,K,V read; O write; LSE write
@@ -166,6 +175,39 @@ class ClockSampler:
                 "source": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
+def env_info():
+    """Where the numbers were taken (report metadata)."""
+    info = {"torch": torch.__version__, "cuda": torch.version.cuda, "nproc": os.cpu_count()}
+    try:
+        info["gpu"] = torch.cuda.get_device_name(0)
+        info["sms"] = torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:
+        pass
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        d = nv.nvmlSystemGetDriverVersion()
+        info["driver"] = d.decode() if isinstance(d, bytes) else d
+    except Exception:
+        pass
+    try:
+        info["git"] = subprocess.run(["git", "rev-parse", "--short", "HEAD"], cwd=ROOT, capture_output=True,
+                                     text=True, timeout=5).stdout.strip() or None
+    except Exception:
+        info["git"] = None
+    if not info.get("git"):
+        try:  # gpurun snapshots have no .git: hash the product sources instead
+            import hashlib
+            h = hashlib.sha1()
+            for root in ("paper_2403_04690_b200/csrc", "include"):
+                for f in sorted(os.listdir(os.path.join(ROOT, root))):
+                    h.update(open(os.path.join(ROOT, root, f), "rb").read())
+            info["src_sha1"] = h.hexdigest()[:12]
+        except Exception:
+            pass
+    return info
+
+
 def init_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -189,9 +231,22 @@ def reduce_max(x: float, world: int, device: str = "cuda") -> float:
     return float(t.item())
 
 
-def shard_range(rank: int, bh_per_rank: int) -> tuple:
-    """Weak scaling: rank r owns global (b,h) slices [r*bh, (r+1)*bh)."""
-    return (rank * bh_per_rank, (rank + 1) * bh_per_rank)
+def shard_range(rank: int, world: int, bh: int) -> tuple:
+    """Strong split: rank g of G owns the flattened (b,h)
+    slices [g*BH/G, (g+1)*BH/G) of a config with BH = B*H slices (floor
+    boundaries, so uneven counts differ by at most one; a rank may own none)."""
+    return (rank * bh // world, (rank + 1) * bh // world)
+
+
+def gather_rows(vals, world: int, device: str = "cuda"):
+    """all_gather of one small fp64 vector per rank -> list of per-rank lists."""
+    if world == 1:
+        return [list(vals)]
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    return [p.tolist() for p in parts]
 
 
 def barrier(world: int):
@@ -203,24 +258,27 @@ def barrier(world: int):
 # ------------------------------------------------------------------ native arm
 
 class Runner:
-    """Buffers and the step function for one rank's batch of the workload."""
+    """Buffers and the step function for one rank's share of the workload:
+    the flattened (b,h) slices shard_range(rank, world, B*H) of config B,
+    passed to the library as batch 1 x heads n (only B*H enters the kernels)."""
 
-    def __init__(self, rank: int):
+    def __init__(self, rank: int, world: int):
         import paper_2403_04690_b200 as na
         self.na = na
         self.cfgs = [na_synth.CONFIGS[v] for v in VARIANTS]
         c = self.cfgs[0]
-        bh = c.batch * c.heads
-        rng = shard_range(rank, bh)  # weak scaling: this rank's own B*H slices
-        q, k, v, do = na_synth.make_inputs(c, device="cuda", bh_range=rng)
-        shape = c.shape()
+        self.bh = shard_range(rank, world, c.batch * c.heads)
+        n = self.bh[1] - self.bh[0]
+        assert n > 0, "every rank owns at least one (b,h) slice of config B"
+        q, k, v, do = na_synth.make_inputs(c, device="cuda", bh_range=self.bh)
+        shape = (1, n, *c.extent, c.head_dim)
         self.q, self.k, self.v, self.do = (t.view(shape) for t in (q, k, v, do))
         self.outs = []
         for cfg in self.cfgs:
             o = torch.empty(shape, dtype=c.dtype, device="cuda")
             lse = torch.empty(shape[:-1], dtype=torch.float32, device="cuda")
             grads = [torch.empty(shape, dtype=c.dtype, device="cuda") for _ in range(3)]
-            pr = na.make_problem(batch=c.batch, heads=c.heads, extent=list(c.extent), head_dim=c.head_dim,
+            pr = na.make_problem(batch=1, heads=n, extent=list(c.extent), head_dim=c.head_dim,
                                  kernel_size=list(cfg.kernel_size), dilation=list(cfg.dilation),
                                  is_causal=[bool(x) for x in cfg.is_causal], dtype=c.dtype)
             ws = torch.empty((na.na_bwd_workspace_size(pr) + 3) // 4, dtype=torch.float32, device="cuda")
@@ -302,80 +360,162 @@ def cpu_baseline_sample():
             "sample": desc + f"; {dt:.1f} s", "seconds": round(dt, 2)}
 
 
-PER_CONFIG = ["B_d1", "B_d1_causal", "B_d4", "B_d4_causal", "C_d1", "C_d8", "D_d2", "E"]
+PER_CONFIG = ["A", "B_d1", "B_d1_causal", "B_d4", "B_d4_causal", "C_d1", "C_d8", "D_d2", "E"]
+# per checked slice: checked, O, LSE, dQ, dK, dV, excess O/dQ/dK/dV, oracle fwd s, oracle bwd s
+_SLICE_FIELDS = 12
+
+
+def slice_check(cfg, host, dev_out, li, stored: bool):
+    """Every token of one (b,h) slice: GPU outputs vs the fp64 oracle's exact
+    forward and gradient (oracle timed while it runs); with `stored`, also
+    dQ/dK against the oracle's stored-O gradient (reading R12).
+    host: the slice's q, k, v, do on the host, shaped [1, X..., D]."""
+    import na_tol
+    import oracle
+    p = oracle.make_problem(1, 1, list(cfg.extent), cfg.head_dim, list(cfg.kernel_size),
+                            list(cfg.dilation), [int(c) for c in cfg.is_causal])
+    hq, hk, hv, hdo = host
+    t0 = time.perf_counter()
+    ro, rlse = oracle.fwd_full_tokens(p, hq, hk, hv)
+    t1 = time.perf_counter()
+    rdq, rdk, rdv = oracle.bwd_gather(p, hq, hk, hv, hdo)
+    t2 = time.perf_counter()
+    o, lse, dq, dk, dv = (t[0, li].float().cpu().numpy() for t in dev_out)
+    N, D = cfg.tokens, cfg.head_dim
+    dt = cfg.dtype
+    ref = [ro.reshape(N, D), rdq.reshape(N, D), rdk.reshape(N, D), rdv.reshape(N, D)]
+    got = [o.reshape(N, D), dq.reshape(N, D), dk.reshape(N, D), dv.reshape(N, D)]
+    row = [1.0, na_tol.max_abs(got[0], ref[0]), na_tol.max_abs(lse.reshape(N), rlse.reshape(N))]
+    row += [na_tol.max_abs(g, r) for g, r in zip(got[1:], ref[1:])]
+    row += [na_tol.excess(g, r, dt) for g, r in zip(got, ref)]
+    row += [t1 - t0, t2 - t1]
+    st = [0.0, 0.0]
+    if stored:
+        sdq, sdk, _ = oracle.bwd_gather(p, hq, hk, hv, hdo, stored_o=True)
+        st = [na_tol.max_abs(got[1], sdq.reshape(N, D)), na_tol.max_abs(got[2], sdk.reshape(N, D))]
+    return row, st
 
 
 def per_config_table(args, world, rank, peaks):
-    """Every BASELINE.json config (SURVEY.md §8(d)): fwd ms and fwd+bwd ms
+    """Every BASELINE.json config (SURVEY.md 8(d)): fwd ms and fwd+bwd ms
     (CUDA events, L2 flushed before each call, max over ranks), effective
-    TFLOP/s with the paper's nominal FLOPs, and the fractions of the B200
-    tensor peak and (forward) of HBM bandwidth.  Weak scaling: each rank owns
-    its own B*H slices of the config (seeded by global slice index)."""
+    TFLOP/s with the paper's nominal FLOPs, the fractions of the B200 tensor
+    peak and (forward) of HBM bandwidth, the kernels' parity on the first and
+    last (b,h) slice, and the oracle's time on them, extrapolated.  Strong
+    split: rank g owns slices shard_range(g, G, B*H) of each config."""
     import paper_2403_04690_b200 as na
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     peak_tf = float(peaks.get("bf16_tflops", 1590.0))
     peak_bw = float(peaks["hbm_gbs"])
     out = {}
-    n = max(3, min(args.steps, 10))
+    n_it = max(3, min(args.steps, 10))
     for name in PER_CONFIG:
         cfg = na_synth.CONFIGS[name]
-        bh = cfg.batch * cfg.heads
-        q, k, v, do = na_synth.make_inputs(cfg, device="cuda", bh_range=shard_range(rank, bh))
-        shape = cfg.shape()
-        q, k, v, do = (t.view(shape) for t in (q, k, v, do))
+        BH = cfg.batch * cfg.heads
+        bh0, bh1 = shard_range(rank, world, BH)
+        n = bh1 - bh0
         kw = dict(kernel_size=list(cfg.kernel_size), dilation=list(cfg.dilation),
                   is_causal=[bool(c) for c in cfg.is_causal])
-        o = torch.empty_like(q)
-        lse = torch.empty(shape[:-1], dtype=torch.float32, device="cuda")
-        dq, dk, dv = (torch.empty_like(q) for _ in range(3))
-        pr = na.make_problem(cfg.batch, cfg.heads, list(cfg.extent), cfg.head_dim, **kw, dtype=cfg.dtype)
-        ws = torch.empty((na.na_bwd_workspace_size(pr) + 3) // 4, dtype=torch.float32, device="cuda")
-
-        def fwd():
-            na.na_fwd(q, k, v, out=o, lse=lse, **kw)
-
-        def fwd_bwd():
-            fwd()
-            na.na_bwd(q, k, v, o, do, lse, dq=dq, dk=dk, dv=dv, workspace=ws, **kw)
-
-        # tile-plan tuning (setup, untimed): rank 0 measures the planner's
-        # candidates, every rank uses its picks (SURVEY §8(f): rank 0 decides)
+        f_ms = fb_ms = 0.0
+        rows = [[0.0] * _SLICE_FIELDS, [0.0] * _SLICE_FIELDS]
+        st = [0.0, 0.0]
+        impl = None
         pick = [0, 0, 0]
-        if rank == 0:
-            pick = list(na.na_tune(q, k, v, do, **kw))
+        if n > 0:
+            shape = (1, n, *cfg.extent, cfg.head_dim)
+            q, k, v, do = (t.view(shape) for t in
+                           na_synth.make_inputs(cfg, device="cuda", bh_range=(bh0, bh1)))
+            o = torch.empty_like(q)
+            lse = torch.empty(shape[:-1], dtype=torch.float32, device="cuda")
+            dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+            pr = na.make_problem(1, n, list(cfg.extent), cfg.head_dim, **kw, dtype=cfg.dtype)
+            impl = {na.NA_IMPL_TC: "tc", na.NA_IMPL_SIMT: "simt"}.get(na.na_selected_impl(pr))
+            ws = torch.empty((na.na_bwd_workspace_size(pr) + 3) // 4, dtype=torch.float32, device="cuda")
+
+            def fwd():
+                na.na_fwd(q, k, v, out=o, lse=lse, **kw)
+
+            def fwd_bwd():
+                fwd()
+                na.na_bwd(q, k, v, o, do, lse, dq=dq, dk=dk, dv=dv, workspace=ws, **kw)
+
+            # tile-plan tuning (setup, untimed): rank 0 measures the planner's
+            # candidates, every rank uses its picks (SURVEY 8(f): rank 0 decides)
+            if rank == 0:
+                pick = list(na.na_tune(q, k, v, do, **kw))
         if world > 1:
             import torch.distributed as dist
             t = torch.tensor(pick, dtype=torch.int32, device="cuda")
             dist.broadcast(t, 0)
             pick = t.tolist()
-        na.na_set_plan_choice(pr, pick)
-        for _ in range(2):
-            fwd_bwd()
-        torch.cuda.synchronize()
+        if n > 0:
+            na.na_set_plan_choice(pr, pick)
+            for _ in range(2):
+                fwd_bwd()
+            torch.cuda.synchronize()
         barrier(world)
-        f_ms = reduce_max(statistics.median(timed_steps(fwd, n, flush)), world)
-        fb_ms = reduce_max(statistics.median(timed_steps(fwd_bwd, n, flush)), world)
-        fl_f = world * flops(cfg, fwd=True, bwd=False)
-        fl_fb = world * flops(cfg)
+        if n > 0:
+            f_ms = statistics.median(timed_steps(fwd, n_it, flush))
+            fb_ms = statistics.median(timed_steps(fwd_bwd, n_it, flush))
+        f_ms = reduce_max(f_ms, world)
+        fb_ms = reduce_max(fb_ms, world)
+        # parity of every token of the config's first and last (b,h) slice,
+        # checked by the rank that owns it (outputs of the last fwd_bwd)
+        if n > 0 and not args.no_parity:
+            outs = (o, lse, dq, dk, dv)
+            for slot, gi in enumerate(sorted({0, BH - 1})):
+                if bh0 <= gi < bh1:
+                    host = [t.view(1, *cfg.extent, cfg.head_dim) for t in
+                            na_synth.make_inputs(cfg, bh_range=(gi, gi + 1))]
+                    rows[slot], s2 = slice_check(cfg, host, outs, gi - bh0, stored=(gi == 0))
+                    if gi == 0:
+                        st = s2
+        allrows = gather_rows(rows[0] + rows[1] + st, world)
+        fl_f = flops(cfg, fwd=True, bwd=False)
+        fl_fb = flops(cfg)
         E = cfg.batch * cfg.heads * cfg.tokens * cfg.head_dim
-        fwd_bytes = world * (4 * E * 2 + 4 * cfg.batch * cfg.heads * cfg.tokens)
-        out[name] = {
+        s_el = 4 if cfg.dtype == torch.float32 else 2
+        fwd_bytes = 4 * E * s_el + 4 * cfg.batch * cfg.heads * cfg.tokens
+        entry = {
             "fwd_ms": round(f_ms, 4), "fwd_bwd_ms": round(fb_ms, 4),
-            "fwd_tflops": round(fl_f / (f_ms * 1e-3) / 1e12, 2),
-            "fwd_bwd_tflops": round(fl_fb / (fb_ms * 1e-3) / 1e12, 2),
-            "fwd_tensor_peak_frac": round(fl_f / (f_ms * 1e-3) / 1e12 / (world * peak_tf), 4),
-            "fwd_bwd_tensor_peak_frac": round(fl_fb / (fb_ms * 1e-3) / 1e12 / (world * peak_tf), 4),
+            "fwd_tflops": round(fl_f / (f_ms * 1e-3) / 1e12, 3),
+            "fwd_bwd_tflops": round(fl_fb / (fb_ms * 1e-3) / 1e12, 3),
+            "fwd_tensor_peak_frac": round(fl_f / (f_ms * 1e-3) / 1e12 / (world * peak_tf), 5),
+            "fwd_bwd_tensor_peak_frac": round(fl_fb / (fb_ms * 1e-3) / 1e12 / (world * peak_tf), 5),
             "fwd_hbm_frac": round(fwd_bytes / (f_ms * 1e-3) / 1e9 / (world * peak_bw), 4),
-            "plan_pick": pick,
+            "plan_pick": pick, "impl": impl, "dtype": str(cfg.dtype).replace("torch.", ""),
         }
-        del q, k, v, do, o, lse, dq, dk, dv, ws
+        checked = [r[k * _SLICE_FIELDS:(k + 1) * _SLICE_FIELDS] for r in allrows for k in range(2)]
+        checked = [c for c in checked if c[0] == 1.0]
+        if checked:
+            mx = lambda i: max(c[i] for c in checked)
+            stored = [max(r[2 * _SLICE_FIELDS + j] for r in allrows) for j in range(2)]
+            excess = max(mx(6), mx(7), mx(8), mx(9))
+            per_slice_f = statistics.mean(c[10] for c in checked)
+            per_slice_b = statistics.mean(c[11] for c in checked)
+            import oracle
+            entry["parity"] = {
+                "slices": sorted({0, BH - 1}), "tokens_per_slice": cfg.tokens, "vs": "oracle exact (fp64)",
+                "max_abs": {"O": mx(1), "LSE": mx(2), "dQ": mx(3), "dK": mx(4), "dV": mx(5)},
+                "max_abs_vs_stored_o": {"dQ": stored[0], "dK": stored[1]},
+                "excess_over_bound": excess, "within_bound": excess <= 0.0,
+                "bound": "max(tol, half-ulp(|ref|)), tol = 1e-2 (16-bit) / 1e-4 (fp32); LSE 2e-3 / 1e-4"}
+            entry["oracle"] = {
+                "fwd_s_per_slice": round(per_slice_f, 3), "bwd_s_per_slice": round(per_slice_b, 3),
+                "slices_timed": len(checked), "cores": oracle.num_threads(),
+                "fwd_bwd_s_whole_config": round((per_slice_f + per_slice_b) * BH, 2),
+                "label": f"extrapolated x{BH} from {len(checked)} slice(s)" if BH > len(checked)
+                         else "measured on the whole config"}
+        out[name] = entry
+        if n > 0:
+            del q, k, v, do, o, lse, dq, dk, dv, ws
         torch.cuda.empty_cache()
     return out
 
 
 def run_native(args, world, rank, local):
     na_peaks, peak_src = load_peaks()
-    R = Runner(rank)
+    R = Runner(rank, world)
     cfg0 = R.cfgs[0]
     step_flops = sum(flops(c) for c in R.cfgs)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2 (126 MB)
@@ -395,7 +535,7 @@ def run_native(args, world, rank, local):
     launches_per_step = R.launches
     ms_rank = sum(per_step) / args.steps
     ms = reduce_max(ms_rank, world)
-    value = world * step_flops / (ms * 1e-3) / 1e12
+    value = step_flops / (ms * 1e-3) / 1e12  # whole config over all ranks (strong split)
 
     # fwd-only timing (for the "fwd ms" half of the metric)
     fwd_ms = reduce_max(sum(timed_steps(R.fwd_only, max(2, args.steps // 2), flush)) /
@@ -417,7 +557,8 @@ def run_native(args, world, rank, local):
     dominant = max(per_kernel, key=lambda n: per_kernel[n][0])
     dom_ms, dom_n = per_kernel[dominant]
     avg_launch_ms = dom_ms / dom_n
-    alg_bytes = algorithmic_bytes(cfg0, dominant)
+    n_local = R.bh[1] - R.bh[0]  # this rank's slices per launch
+    alg_bytes = algorithmic_bytes(cfg0, dominant, n_local)
     achieved = alg_bytes / (avg_launch_ms * 1e-3) / 1e9
     peak = float(na_peaks["hbm_gbs"])
     traffic = None
@@ -435,7 +576,7 @@ def run_native(args, world, rank, local):
         ms_avg = tot / cnt
         key = "fna_bwd_pre" if n.startswith("fna_bwd_pre") else n
         try:
-            gbs = algorithmic_bytes(cfg0, key) / (ms_avg * 1e-3) / 1e9
+            gbs = algorithmic_bytes(cfg0, key, n_local) / (ms_avg * 1e-3) / 1e9
         except KeyError:
             continue
         per_kernel_roof[n] = {"avg_launch_ms": round(ms_avg, 5), "achieved_gbs": round(gbs, 1),
@@ -464,7 +605,7 @@ def run_native(args, world, rank, local):
         e_ms = reduce_max(sum(timed_steps(e2e_step, n_e2e)) / n_e2e, world)
         h2d = sum(t.numel() * t.element_size() for t in host)
         d2h = sum(t.numel() * t.element_size() for hs in outs_host for t in hs)
-        e2e = {"value": world * step_flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+        e2e = {"value": step_flops / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
     per_config = None
@@ -483,11 +624,13 @@ def run_native(args, world, rank, local):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
         "data": "synthetic unit-normal Q,K,V,dO (seeded per (b,h)); no weights",
-        "config": {"workload": WORKLOAD, "variants": VARIANTS, "batch_per_gpu": cfg0.batch,
+        "config": {"workload": WORKLOAD, "variants": VARIANTS, "batch": cfg0.batch,
                    "heads": cfg0.heads, "seq_len": cfg0.tokens, "head_dim": cfg0.head_dim,
-                   "kernel_size": 255, "parallelism": f"bxh-shard x{world} (weak)",
+                   "kernel_size": 255,
+                   "parallelism": f"B*H split over {world} GPU(s): rank g owns slices "
+                                  f"[g*{cfg0.batch * cfg0.heads}/{world}, (g+1)*{cfg0.batch * cfg0.heads}/{world})",
                    "l2": "inputs 1.07 GB/step > 126 MB L2, plus a 256 MB L2 flush between steps "
                          "outside the timed events"},
         "fwd_ms_per_step": round(fwd_ms, 4),
@@ -501,6 +644,7 @@ def run_native(args, world, rank, local):
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
+        "env": env_info(),
     }
     print(json.dumps(line), flush=True)
 
@@ -543,6 +687,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-config", action="store_true",
                     help="skip the fwd / fwd+bwd table of every BASELINE.json config")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the per-config whole-slice oracle parity (and oracle timing)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -87,6 +87,7 @@ def lib():
             L.nar_fwd.argtypes = [P, ctypes.c_int, vp, vp, vp, dp, dp]
             L.nar_fwd_tokens.argtypes = [P, ctypes.c_int, vp, vp, vp, i64, vp, dp, dp]
             L.nar_bwd.argtypes = [P, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, dp, dp, dp]
+            L.nar_bwd_gather.argtypes = [P, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, dp, dp, dp]
             L.nar_bwd_tokens.argtypes = [P, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, i64, vp, dp, dp,
                                          dp]
             _lib = L
@@ -186,6 +187,28 @@ def bwd(p: Problem, q, k, v, d_o, stored_o: bool = False):
     if rc:
         raise ValueError(f"oracle rejected problem (code {rc})")
     return tuple(o.reshape(p.batch, p.heads, N, D) for o in outs)
+
+
+def bwd_gather(p: Problem, q, k, v, d_o, stored_o: bool = False):
+    """Full backward in gather form (parallel over tokens; for whole-slice
+    checks of large problems).  Same result as bwd() up to fp64 summation
+    order; returns (dQ, dK, dV), each [B,H,N,D] fp64."""
+    (bq, bk, bv, bo), code = _prep(q, k, v, d_o)
+    N, BH, D = _tokens(p), p.batch * p.heads, p.head_dim
+    outs = [np.empty((BH * N * D,), np.float64) for _ in range(3)]
+    rc = lib().nar_bwd_gather(ctypes.byref(p), code, code if stored_o else F64, bq[2], bk[2], bv[2],
+                              bo[2], *map(_ptr, outs))
+    if rc:
+        raise ValueError(f"oracle rejected problem (code {rc})")
+    return tuple(o.reshape(p.batch, p.heads, N, D) for o in outs)
+
+
+def fwd_full_tokens(p: Problem, q, k, v):
+    """Full forward via the token form (parallel over tokens rather than
+    slices); returns (O [B,H,N,D], LSE [B,H,N])."""
+    N, BH, D = _tokens(p), p.batch * p.heads, p.head_dim
+    o, lse = fwd_tokens(p, q, k, v, np.arange(BH * N, dtype=np.int64))
+    return o.reshape(p.batch, p.heads, N, D), lse.reshape(p.batch, p.heads, N)
 
 
 def bwd_tokens(p: Problem, q, k, v, d_o, tokens, stored_o: bool = False):

@@ -356,6 +356,81 @@ int nar_bwd_tokens(const nar_problem* p, int dtype, int o_dtype, const void* q, 
   return 0;
 }
 
+int nar_bwd_gather(const nar_problem* p, int dtype, int o_dtype, const void* q, const void* k,
+                   const void* v, const void* d_o, double* dq, double* dk, double* dv) {
+  int rc = nar_check(p);
+  if (rc) return rc;
+  const int64_t N = tokens_per_slice(p), BH = (int64_t)p->batch * p->heads;
+  const int D = p->head_dim;
+  const int64_t L = max_window(p);
+  const double scale = scale_of(p);
+  double* lse = (double*)malloc(sizeof(double) * N);
+  double* Dvec = (double*)malloc(sizeof(double) * N);
+  for (int64_t bh = 0; bh < BH; ++bh) {
+    /* queries: LSE_x, D_x = <dO_x, O_x>, dQ_x = scale sum_y P_xy (dP_xy - D_x) k_y */
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t x = 0; x < N; ++x) {
+      int64_t* keys = (int64_t*)malloc(sizeof(int64_t) * L);
+      double* prob = (double*)malloc(sizeof(double) * L);
+      double* o_row = (double*)malloc(sizeof(double) * D);
+      int nk;
+      lse[x] = forward_row(p, dtype, q, k, v, bh, x, keys, prob, &nk, o_row);
+      const int64_t xo = (bh * N + x) * D;
+      double Dx = 0.0;
+      for (int d = 0; d < D; ++d) Dx += load(dtype, d_o, xo + d) * stored(o_dtype, o_row[d]);
+      Dvec[x] = Dx;
+      for (int d = 0; d < D; ++d) dq[xo + d] = 0.0;
+      for (int j = 0; j < nk; ++j) {
+        const int64_t yo = (bh * N + keys[j]) * D;
+        double dP = 0.0;
+        for (int d = 0; d < D; ++d) dP += load(dtype, d_o, xo + d) * load(dtype, v, yo + d);
+        const double dS = prob[j] * (dP - Dx);
+        for (int d = 0; d < D; ++d) dq[xo + d] += scale * dS * load(dtype, k, yo + d);
+      }
+      free(keys);
+      free(prob);
+      free(o_row);
+    }
+    /* keys: dK_t = scale sum_{x: t in N(x)} dS_xt q_x, dV_t = sum P_xt dO_x.
+     * The queries with t in N(x) lie within (k-1)*dil of t on each axis
+     * (see nar_bwd_tokens); membership is tested with the forward rule. */
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t t = 0; t < N; ++t) {
+      const int64_t to = (bh * N + t) * D;
+      for (int d = 0; d < D; ++d) dk[to + d] = dv[to + d] = 0.0;
+      int ct[3], lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+      unflatten(p, t, ct);
+      for (int a = 0; a < p->rank; ++a) {
+        const int reach = (p->kernel_size[a] - 1) * p->dilation[a];
+        lo[a] = ct[a] - reach < 0 ? 0 : ct[a] - reach;
+        hi[a] = ct[a] + reach > p->extent[a] - 1 ? p->extent[a] - 1 : ct[a] + reach;
+      }
+      int c[3] = {0, 0, 0};
+      for (c[0] = lo[0]; c[0] <= hi[0]; ++c[0])
+        for (c[1] = lo[1]; c[1] <= hi[1]; ++c[1])
+          for (c[2] = lo[2]; c[2] <= hi[2]; ++c[2]) {
+            const int64_t x = flatten(p, c);
+            if (!nar_contains(p, x, t)) continue;
+            const int64_t xo = (bh * N + x) * D;
+            double s = 0.0, dP = 0.0;
+            for (int d = 0; d < D; ++d) {
+              s += load(dtype, q, xo + d) * load(dtype, k, to + d);
+              dP += load(dtype, d_o, xo + d) * load(dtype, v, to + d);
+            }
+            const double P = exp(scale * s - lse[x]);      /* P_xt */
+            const double dS = P * (dP - Dvec[x]);            /* dS_xt */
+            for (int d = 0; d < D; ++d) {
+              dk[to + d] += scale * dS * load(dtype, q, xo + d);
+              dv[to + d] += P * load(dtype, d_o, xo + d);
+            }
+          }
+    }
+  }
+  free(lse);
+  free(Dvec);
+  return 0;
+}
+
 int nar_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -84,6 +84,17 @@ int nar_bwd_tokens(const nar_problem* p, int dtype, int o_dtype, const void* q, 
                    const void* v, const void* d_o, int64_t n, const int64_t* tokens,
                    double* dq, double* dk, double* dv);
 
+/* Full backward in gather form, every token of every slice, parallel over
+ * tokens (for whole-slice checks of large problems, where nar_bwd's
+ * per-slice parallelism leaves cores idle).  Per slice: one pass over the
+ * queries x computes LSE_x, D_x = <dO_x, O_x> (o_dtype as in nar_bwd) and
+ * dQ_x; a second pass over the keys t gathers dK_t, dV_t from the queries
+ * {x : t in N(x)} with P_xt = exp(s_xt - LSE_x) (the same expression
+ * forward_row uses), so the result is nar_bwd's up to fp64 summation order.
+ * Outputs [B,H,N,D]. */
+int nar_bwd_gather(const nar_problem* p, int dtype, int o_dtype, const void* q, const void* k,
+                   const void* v, const void* d_o, double* dq, double* dk, double* dv);
+
 /* Threads the OpenMP runtime will use (for reporting `cores`). */
 int nar_num_threads(void);
 

@@ -311,41 +311,49 @@ na_status na_tune(const na_problem* p, const void* q, const void* k, const void*
   int32_t best[3] = {0, 0, 0};
   if (n > 1) {
     // Time every candidate plan for each kernel (forward, dK/dV, dQ) with
-    // the launch-event hook, keep the fastest per kernel.  The caller's own
-    // profiling state is set aside meanwhile.
+    // the launch-event hook, keep the fastest per kernel.  Candidates run
+    // under a plan override local to this thread, so the process-wide table
+    // (and other threads) never see a transient pick; it changes only once,
+    // at the end, to the winners.  The caller's own profiling state is set
+    // aside meanwhile.  A candidate whose timing fails counts as +inf.
     const bool prof_saved = g_prof;
     std::vector<ProfEntry> list_saved;
     list_saved.swap(g_prof_list);
-    float best_ms[3] = {1e30f, 1e30f, 1e30f};
+    float best_ms[3] = {INFINITY, INFINITY, INFINITY};
     for (int c = 0; c < n && s == NA_OK; ++c) {
-      const int32_t pick[3] = {c, c, c};
-      s = na_set_plan_choice(p, pick);
+      const na::PlanChoice pick{c, c, c};
+      na::set_plan_override(&pick);
       for (int it = 0; it < 3 && s == NA_OK; ++it) {
         g_prof = it > 0;  // first pass warms up
         s = na_fwd(p, q, k, v, o, lse, stream);
         if (s == NA_OK)
           s = na_bwd(p, q, k, v, o, d_o, lse, dq, dk, dv, workspace, workspace_bytes, stream);
       }
+      na::set_plan_override(nullptr);
       g_prof = false;
       float sum[3] = {0.f, 0.f, 0.f};
+      bool ok[3] = {true, true, true};
       for (ProfEntry& e : g_prof_list) {
         float t = 0.f;
-        if (cudaEventSynchronize(e.b) == cudaSuccess) cudaEventElapsedTime(&t, e.a, e.b);
+        const bool good = cudaEventSynchronize(e.b) == cudaSuccess && cudaEventElapsedTime(&t, e.a, e.b) == cudaSuccess;
         const int slot = e.id == na::KID_FWD_TC ? 0 : e.id == na::KID_DKDV_TC ? 1 : e.id == na::KID_DQ_TC ? 2 : -1;
-        if (slot >= 0) sum[slot] += t;
+        if (slot >= 0) {
+          sum[slot] += t;
+          ok[slot] = ok[slot] && good;
+        }
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
       }
       g_prof_list.clear();
       for (int i = 0; i < 3; ++i)
-        if (sum[i] < best_ms[i]) {
+        if (ok[i] && sum[i] > 0.f && sum[i] < best_ms[i]) {
           best_ms[i] = sum[i];
           best[i] = c;
         }
     }
     g_prof = prof_saved;
     g_prof_list.swap(list_saved);
-    if (s != NA_OK) return s;
+    if (s != NA_OK) return s;  // the table still holds the previous picks
     s = na_set_plan_choice(p, best);
     if (s != NA_OK) return s;
   }

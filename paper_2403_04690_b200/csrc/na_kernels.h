@@ -41,11 +41,18 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
 // tcgen05 path.  tc_supported() is a pure host check; the launchers return
 // cudaErrorNotSupported for problems outside it.
 bool tc_supported(int dtype, const Geom& g, const char** why);
+// Opt a kernel into `bytes` of dynamic shared memory on the current device
+// (once per kernel and device; thread-safe).
+cudaError_t ensure_smem_attr(const void* func, int bytes);
 // Candidate plans of the tile planner for g (1 for rank 1), and the measured
 // choice per kernel (tc_host.cpp; na_tune sets it).
 int tc_plan_candidates(const Geom& g);
 PlanChoice plan_choice(const Geom& g, int dtype);
 void set_plan_choice(const Geom& g, int dtype, PlanChoice c);
+// Calling thread only: every plan_choice() returns *c (nullptr: off).  na_tune
+// times candidates with it, so the process-wide table never holds a
+// transient pick.
+void set_plan_override(const PlanChoice* c);
 cudaError_t tc_fwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
                    void* o, float* lse, cudaStream_t st, int* launches);
 cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,

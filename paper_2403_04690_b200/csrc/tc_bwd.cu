@@ -67,7 +67,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 // Both kernels stream 4 stages; a fused dQ (FUSE: rank 1) holds the O tiles
 // it reads to form the row vectors itself (see the dQ compute warps) where
 // dK/dV keeps the gathered row vectors of its streamed chunks.
-template <int D, bool KV, bool FUSE>
+template <int D, bool KV, bool FUSE, bool EXACT = false>
 struct BwdSmem {
   static constexpr int kSt = 4;                       // streamed stages
   static constexpr int kRowBytes = D * 2;
@@ -78,7 +78,8 @@ struct BwdSmem {
   static constexpr int kB1 = kB0 + kSt * kTile;       // streamed [kSt] (dO | V)
   static constexpr int kVec = kB1 + kSt * kTile;      // [kSt][-LSE2 x128 | D x128] fp32 (dK/dV)
   static constexpr int kBar = kVec + (KV ? kSt * 256 * 4 : 0);
-  static constexpr int kBytes = kBar + 256;
+  static constexpr int kDx = kBar + 256;              // exact-D dQ: [2 groups][128] fp32 partials
+  static constexpr int kBytes = kDx + (EXACT ? 2 * 128 * 4 : 0);
 };
 
 // TMEM columns (512): three sub-chunk buffers b = gu % 3 at [128b, 128b + 128):
@@ -101,7 +102,9 @@ enum : int {
   B_PE = B_P + 3,           // OUT MMAs of the buffer's sub-chunk done: buffer free [3]
   B_OF = B_PE + 3,          // outputs of a tile final [2]
   B_OE = B_OF + 2,          // outputs drained [2]
-  B_COUNT = B_OE + 2
+  B_DX = B_OE + 2,          // exact-D dQ: both groups' partial sums of the tile written (256 arrivals)
+  B_DXE = B_DX + 1,         // exact-D dQ: partials read by both groups' epilogues (256 arrivals)
+  B_COUNT = B_DXE + 1
 };
 
 // Tensor maps of one backward kernel: stationary tiles a0, a1; streamed
@@ -125,10 +128,27 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   // multi-dimensional tiles the extra per-tile work measured slower than the
   // separate preprocess pass, so there dQ reads them.
   constexpr bool kFuse = !KV_STATIONARY && RANK == 1;
-  using S = BwdSmem<D, KV_STATIONARY, kFuse>;
+  // bf16 dQ (R12): D_x is corrected in-kernel to sum_y P_xy dP_xy.
+  // The row value read at the tile start, Dt_x = <dO_x, O_x> from the
+  // stored (bf16-rounded) O, is only an estimate; the compute warps also
+  // sum c_x = sum_y dS_xy = sum_y P_xy (dP_xy - Dt_x) = D_x - Dt_x in fp32
+  // (the P_xy of a row sum to 1), and a second OUT MMA accumulates
+  // PK_x = sum_y P_xy k_y next to dQ, so the epilogue forms
+  //   dQ_x = scale (sum_y P_xy (dP_xy - Dt_x) k_y - c_x PK_x)
+  // = scale sum_y P_xy (dP_xy - D_x) k_y, and writes D_x = Dt_x + c_x to the
+  // row vectors the dK/dV kernel (run next) reads.  Dt_x keeps the large
+  // first term free of cancellation; c_x is small.  fp16's stored O is 8x
+  // finer and keeps Dt_x.
+  constexpr bool kExactD = !KV_STATIONARY && BF16;
+  // bf16 (R13): the 16-bit A operands of the OUT MMAs (P, dS) are
+  // split hi + lo, x = bf16(x) + bf16(x - bf16(x)), and both halves are
+  // multiplied (a second MMA into the same accumulator), so the products
+  // carry ~2^-17 instead of 2^-9 relative error; fp16's 2^-12 needs no split.
+  constexpr bool kSplit = BF16;
+  using S = BwdSmem<D, KV_STATIONARY, kFuse, kExactD>;
   constexpr int kStages = S::kSt;
   // Output accumulator columns per tile; double-buffered when two fit.
-  constexpr int kOutCols = KV_STATIONARY ? 2 * D : D;
+  constexpr int kOutCols = (KV_STATIONARY || kExactD) ? 2 * D : D;
   constexpr bool kOutDouble = 2 * kOutCols <= 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned by pointer arithmetic on the __shared__ array, so the
@@ -147,6 +167,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       ptx::mbar_init(bar + B_OF + b, 1);
       ptx::mbar_init(bar + B_OE + b, KV_STATIONARY ? 128 : kCompute);
     }
+    ptx::mbar_init(bar + B_DX, kCompute);
+    ptx::mbar_init(bar + B_DXE, kCompute);
     for (int b = 0; b < 3; ++b) {
       ptx::mbar_init(bar + B_S + b, 1);
       ptx::mbar_init(bar + B_P + b, 128);
@@ -346,16 +368,24 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           for (int kk = 0; kk < width / 16; ++kk) {
             const uint32_t boff = kk * 16 * S::kRowBytes;
             const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
+            // packed A operand columns of K-step kk (16 partner columns):
+            // contiguous for fp16; bf16 keeps hi at +0 and lo at +16 of each
+            // 32-column half (see the compute warps)
+            const uint32_t ca = kSplit ? 32 * (kk >> 1) + 8 * (kk & 1) : 8 * kk;
             if constexpr (KV_STATIONARY) {
-              // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
-              ptx::mma_ts_w(tmem + out + D, pk + kk * 8,
-                            ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
-              ptx::mma_ts_w(tmem + out, pk + 64 + kk * 8,
-                            ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+              // dV += P^T dO ; dK += dS^T Q   (B operands MN-major; bf16: hi + lo)
+              const uint64_t dod = ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw);
+              const uint64_t qd = ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw);
+              ptx::mma_ts_w(tmem + out + D, pk + ca, dod, idesc_o, acc);
+              if constexpr (kSplit) ptx::mma_ts_w(tmem + out + D, pk + ca + 16, dod, idesc_o, 1u);
+              ptx::mma_ts_w(tmem + out, pk + 64 + ca, qd, idesc_o, acc);
+              if constexpr (kSplit) ptx::mma_ts_w(tmem + out, pk + 64 + ca + 16, qd, idesc_o, 1u);
             } else {
-              // dQ += dS K
-              ptx::mma_ts_w(tmem + out, pk + 64 + kk * 8,
-                            ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw), idesc_o, acc);
+              // dQ += dS K (bf16: hi + lo), exact-D: PK += P K (same B operand)
+              const uint64_t kd = ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw);
+              ptx::mma_ts_w(tmem + out, pk + 64 + ca, kd, idesc_o, acc);
+              if constexpr (kSplit) ptx::mma_ts_w(tmem + out, pk + 64 + ca + 16, kd, idesc_o, 1u);
+              if constexpr (kExactD) ptx::mma_ts_w(tmem + out + D, pk + ca, kd, idesc_o, acc);
             }
           }
           ptx::mma_commit_w(bar + B_PE + b3);
@@ -492,6 +522,36 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
             make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
     };
+    // Exact-D dQ drain: (dQacc - c_x PK_x) * scale, 16 columns per round trip.
+    auto drain_exact = [&](uint32_t src, uint32_t src_pk, uint8_t* stage, int col0, int ncols, float mul,
+                           float corr) {
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
+        uint32_t ov[16], kv_[16];
+        NA_TMEM_LD16(trow + src + c0, ov);
+        NA_TMEM_LD16(trow + src_pk + c0, kv_);
+        ptx::tmem_ld_wait();
+        uint32_t pk[8];
+#pragma unroll
+        for (int c = 0; c < 16; c += 2)
+          pk[c >> 1] = pack2<BF16>((__uint_as_float(ov[c]) - corr * __uint_as_float(kv_[c])) * mul,
+                                   (__uint_as_float(ov[c + 1]) - corr * __uint_as_float(kv_[c + 1])) * mul);
+        const int chunk = (col0 + c0) / 8;
+        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk, S::kRowBytes)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + 1, S::kRowBytes)) =
+            make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    };
+    float* dx_part = reinterpret_cast<float*>(smem + S::kDx);  // exact-D: [2 groups][128 rows]
+    long long prow_rv = -1;  // exact-D: row-vector index of this row in the pending tile (-1: invalid row)
+    float prow_d = 0.f;      // exact-D: its Dt_x
+    auto rv_index = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r) -> long long {
+      if (!r.valid) return -1;
+      long long i = rv_base(g, t.bh, t.res);
+#pragma unroll
+      for (int a = 0; a < RANK; ++a) i += (long long)r.c[a] * g.rv_cs[a];
+      return i;
+    };
     auto epilogue = [&](const TileCtx<RANK>& t, uint32_t tix) {
       const int ob = kOutDouble ? (tix & 1) : 0, ab = tix & 1;
       ptx::mbar_wait(bar + B_OF + ob, kOutDouble ? ((tix >> 1) & 1) : (tix & 1));
@@ -502,6 +562,12 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       if constexpr (KV_STATIONARY) {
         drain(src, stage0, 0, D, g.scale);                 // dK -> K tile
         drain(src + D, stage0 + S::kTile, 0, D, 1.f);      // dV -> V tile
+      } else if constexpr (kExactD) {
+        ptx::mbar_wait(bar + B_DX, tix & 1);  // both groups' c_x partials of the tile
+        const float corr = dx_part[row] + dx_part[128 + row];
+        ptx::mbar_arrive(bar + B_DXE);
+        drain_exact(src + grp * (D / 2), src + D + grp * (D / 2), stage0, grp * (D / 2), D / 2, g.scale, corr);
+        if (grp == 0 && prow_rv >= 0) rv[prow_rv + g.rv_plane] = prow_d + corr;  // D_x for dK/dV
       } else {
         drain(src + grp * (D / 2), stage0, grp * (D / 2), D / 2, g.scale);  // half of dQ -> Q tile
       }
@@ -568,6 +634,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       if (u_first / ns) t.next_origin(pl, org);
       uint32_t w[2];
       r.sub_mask(pl, org, u_first % ns, w);
+      float2 dxacc = make_float2(0.f, 0.f);  // exact-D: this group's part of c_x = sum_y dS_xy
       for (int u = u_first; u < nsub; u += 2) {
         if (issuer && u != u_first) release_store();  // the store has had a sub-chunk to read
         const uint32_t gu = ub + u;
@@ -616,52 +683,95 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           }
           ptx::tmem_ld_wait();
           if (tracer) NA_TRACE_EV(2 + grp, tr, 26 + 2 * gq);
-          if (!any) {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) pk_p[gq][c] = pk_s[gq][c] = 0u;
-          } else {
+          // P and dS of 4 partner columns c..c+3 (fp32 pairs)
+          auto calc4 = [&](int c, bool full, float2& p0, float2& p1, float2& ds0, float2& ds1) {
+            float4 nl4, dd4;
+            if constexpr (KV_STATIONARY) {
+              nl4 = *reinterpret_cast<const float4*>(cl + 32 * gq + c);
+              dd4 = *reinterpret_cast<const float4*>(cd + 32 * gq + c);
+            } else {
+              nl4 = make_float4(row_nl2, row_nl2, row_nl2, row_nl2);
+              dd4 = make_float4(row_d, row_d, row_d, row_d);
+            }
+            float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])),
+                                   make_float2(sl2, sl2), make_float2(nl4.x, nl4.y));
+            float2 x1 = __ffma2_rn(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])),
+                                   make_float2(sl2, sl2), make_float2(nl4.z, nl4.w));
+            if (!full) {
+              const uint32_t ww = w[gq];
+              x0.x = (ww >> c) & 1u ? x0.x : -INFINITY;
+              x0.y = (ww >> (c + 1)) & 1u ? x0.y : -INFINITY;
+              x1.x = (ww >> (c + 2)) & 1u ? x1.x : -INFINITY;
+              x1.y = (ww >> (c + 3)) & 1u ? x1.y : -INFINITY;
+            }
+            p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
+            p1 = use_poly(c) ? exp2_poly2(x1)                   // FMA pipe
+                             : make_float2(ptx::ex2(x1.x), ptx::ex2(x1.y));
+            ds0 = __fmul2_rn(p0, __fadd2_rn(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])),
+                                            make_float2(-dd4.x, -dd4.y)));
+            ds1 = __fmul2_rn(p1, __fadd2_rn(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])),
+                                            make_float2(-dd4.z, -dd4.w)));
+            if constexpr (kExactD) dxacc = __fadd2_rn(dxacc, __fadd2_rn(ds0, ds1));
+          };
+          if constexpr (kSplit) {
+            // bf16: per 16 partner columns j, hi words at +8j and lo words at
+            // +16+8j of this half's 32 columns, over S (P) and dP (dS), which
+            // this half has already loaded.
             const bool full = __all_sync(0xffffffffu, w[gq] == 0xffffffffu);
 #pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-              float4 nl4, dd4;
-              if constexpr (KV_STATIONARY) {
-                nl4 = *reinterpret_cast<const float4*>(cl + 32 * gq + c);
-                dd4 = *reinterpret_cast<const float4*>(cd + 32 * gq + c);
+            for (int j = 0; j < 2; ++j) {
+              uint32_t ph[8], pl[8], sh[8], sl[8];
+              if (!any) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ph[i] = pl[i] = sh[i] = sl[i] = 0u;
               } else {
-                nl4 = make_float4(row_nl2, row_nl2, row_nl2, row_nl2);
-                dd4 = make_float4(row_d, row_d, row_d, row_d);
+#pragma unroll
+                for (int c = 16 * j; c < 16 * j + 16; c += 4) {
+                  float2 p0, p1, ds0, ds1;
+                  calc4(c, full, p0, p1, ds0, ds1);
+                  const int i = (c - 16 * j) >> 1;
+                  ph[i] = pack2<BF16>(p0.x, p0.y);
+                  ph[i + 1] = pack2<BF16>(p1.x, p1.y);
+                  sh[i] = pack2<BF16>(ds0.x, ds0.y);
+                  sh[i + 1] = pack2<BF16>(ds1.x, ds1.y);
+                  const float2 r0 = __ffma2_rn(unpack2<BF16>(ph[i]), make_float2(-1.f, -1.f), p0);
+                  const float2 r1 = __ffma2_rn(unpack2<BF16>(ph[i + 1]), make_float2(-1.f, -1.f), p1);
+                  const float2 t0 = __ffma2_rn(unpack2<BF16>(sh[i]), make_float2(-1.f, -1.f), ds0);
+                  const float2 t1 = __ffma2_rn(unpack2<BF16>(sh[i + 1]), make_float2(-1.f, -1.f), ds1);
+                  pl[i] = pack2<BF16>(r0.x, r0.y);
+                  pl[i + 1] = pack2<BF16>(r1.x, r1.y);
+                  sl[i] = pack2<BF16>(t0.x, t0.y);
+                  sl[i + 1] = pack2<BF16>(t1.x, t1.y);
+                }
               }
-              float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])),
-                                     make_float2(sl2, sl2), make_float2(nl4.x, nl4.y));
-              float2 x1 = __ffma2_rn(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])),
-                                     make_float2(sl2, sl2), make_float2(nl4.z, nl4.w));
-              if (!full) {
-                const uint32_t ww = w[gq];
-                x0.x = (ww >> c) & 1u ? x0.x : -INFINITY;
-                x0.y = (ww >> (c + 1)) & 1u ? x0.y : -INFINITY;
-                x1.x = (ww >> (c + 2)) & 1u ? x1.x : -INFINITY;
-                x1.y = (ww >> (c + 3)) & 1u ? x1.y : -INFINITY;
-              }
-              const float2 p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
-              const float2 p1 = use_poly(c) ? exp2_poly2(x1)                   // FMA pipe
-                                            : make_float2(ptx::ex2(x1.x), ptx::ex2(x1.y));
-              const float2 ds0 = __fmul2_rn(
-                  p0, __fadd2_rn(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])),
-                                 make_float2(-dd4.x, -dd4.y)));
-              const float2 ds1 = __fmul2_rn(
-                  p1, __fadd2_rn(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])),
-                                 make_float2(-dd4.z, -dd4.w)));
-              pk_p[gq][c >> 1] = pack2<BF16>(p0.x, p0.y);
-              pk_p[gq][(c >> 1) + 1] = pack2<BF16>(p1.x, p1.y);
-              pk_s[gq][c >> 1] = pack2<BF16>(ds0.x, ds0.y);
-              pk_s[gq][(c >> 1) + 1] = pack2<BF16>(ds1.x, ds1.y);
+              const uint32_t a = pk + 32 * gq + 8 * j;
+              NA_TMEM_ST8(a + 64, sh);       // dS (dS^T) hi
+              NA_TMEM_ST8(a + 64 + 16, sl);  // dS lo
+              NA_TMEM_ST8(a, ph);            // P (P^T) hi
+              if constexpr (KV_STATIONARY) NA_TMEM_ST8(a + 16, pl);  // P^T lo (dV); dQ's PK needs no lo
             }
-          }
-          if constexpr (KV_STATIONARY) {
-            NA_TMEM_ST16(pk + 16 * gq, pk_p[gq]);       // P^T  -> A of dV += P^T dO
-            NA_TMEM_ST16(pk + 64 + 16 * gq, pk_s[gq]);  // dS^T -> A of dK += dS^T Q
           } else {
-            NA_TMEM_ST16(pk + 64 + 16 * gq, pk_s[gq]);  // dS -> A of dQ += dS K
+            if (!any) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) pk_p[gq][c] = pk_s[gq][c] = 0u;
+            } else {
+              const bool full = __all_sync(0xffffffffu, w[gq] == 0xffffffffu);
+#pragma unroll
+              for (int c = 0; c < 32; c += 4) {
+                float2 p0, p1, ds0, ds1;
+                calc4(c, full, p0, p1, ds0, ds1);
+                pk_p[gq][c >> 1] = pack2<BF16>(p0.x, p0.y);
+                pk_p[gq][(c >> 1) + 1] = pack2<BF16>(p1.x, p1.y);
+                pk_s[gq][c >> 1] = pack2<BF16>(ds0.x, ds0.y);
+                pk_s[gq][(c >> 1) + 1] = pack2<BF16>(ds1.x, ds1.y);
+              }
+            }
+            if constexpr (KV_STATIONARY) {
+              NA_TMEM_ST16(pk + 16 * gq, pk_p[gq]);       // P^T  -> A of dV += P^T dO
+              NA_TMEM_ST16(pk + 64 + 16 * gq, pk_s[gq]);  // dS^T -> A of dK += dS^T Q
+            } else {
+              NA_TMEM_ST16(pk + 64 + 16 * gq, pk_s[gq]);  // dS -> A of dQ += dS K
+            }
           }
           if (tracer) NA_TRACE_EV(2 + grp, tr, 27 + 2 * gq);
         }
@@ -684,6 +794,15 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           epilogue(tp, ti - 1);
           pend = false;
         }
+      }
+      if constexpr (kExactD) {
+        // publish this group's c_x partial once both epilogues have read the
+        // previous tile's (single slot)
+        if (ti > 0) ptx::mbar_wait(bar + B_DXE, (ti - 1) & 1);
+        dx_part[grp * 128 + row] = dxacc.x + dxacc.y;
+        ptx::mbar_arrive(bar + B_DX);
+        prow_rv = rv_index(t, r);
+        prow_d = row_d;
       }
       if (issuer) release_store();
       tp = t;
@@ -746,33 +865,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   bwd_body<RANK, D, BF16, false>(maps, g, pl, rv, lse, num_tiles);
 }
 
+// Everything that can fail on the host (function attributes; the tensor maps
+// are encoded by the caller) happens before the first launch, so an error
+// leaves the stream and the workspace untouched (include/na.h).
 template <int RANK, int D, bool BF16>
-cudaError_t launch_both(const Geom& g, const TcPlan* pls, const BwdMaps& mkv, const BwdMaps& mq,
-                        float* rv, const float* lse, cudaStream_t st) {
+cudaError_t launch_all(int dtype, const Geom& g, const TcPlan* pls, const BwdMaps& mkv, const BwdMaps& mq,
+                       const void* o, const void* d_o, float* rv, const float* lse, cudaStream_t st) {
   constexpr bool kFuse = RANK == 1;  // dQ forms the row vectors (see bwd_body)
   const int smem_kv = BwdSmem<D, true, false>::kBytes + 1024;
-  const int smem_q = BwdSmem<D, false, kFuse>::kBytes + 1024;
+  const int smem_q = BwdSmem<D, false, kFuse, BF16>::kBytes + 1024;
   auto kdkdv = fna_dkdv_tc<RANK, D, BF16>;
   auto kdq = fna_dq_tc<RANK, D, BF16>;
-  static bool attr = false;  // benign race: idempotent
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kdkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kdq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kdkdv), smem_kv);
+  if (e != cudaSuccess) return e;
+  if ((e = ensure_smem_attr(reinterpret_cast<const void*>(kdq), smem_q)) != cudaSuccess) return e;
   const long long tiles_kv = (long long)g.BH * pls[0].nres * pls[0].tiles;
   const long long tiles_q = (long long)g.BH * pls[1].nres * pls[1].tiles;
   if (tiles_kv > 0x7fffffffLL || tiles_q > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const unsigned grid_kv = (unsigned)(tiles_kv < num_sms() ? tiles_kv : num_sms());
   const unsigned grid_q = (unsigned)(tiles_q < num_sms() ? tiles_q : num_sms());
+  // Row-vector layout: rank 1, written by the dQ kernel (fused preprocess;
+  // slots no token maps to, ragged residue classes, must read as 0);
+  // otherwise by the preprocess kernel.
+  e = kFuse ? rv_clear_padding(g, rv, st) : bwd_preprocess(dtype, g, o, d_o, lse, rv, st);
+  if (e != cudaSuccess) return e;
   // dQ first: when fused it also writes the row vectors (-LSE*log2(e), D)
   // the dK/dV kernel streams.
   prof_begin(KID_DQ_TC, st);
   kdq<<<grid_q, kThreads, smem_q, st>>>(mq, g, pls[1], rv, lse, (unsigned)tiles_q);
   prof_end(st);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   prof_begin(KID_DKDV_TC, st);
   kdkdv<<<grid_kv, kThreads, smem_kv, st>>>(mkv, g, pls[0], rv, (unsigned)tiles_kv);
@@ -782,13 +904,13 @@ cudaError_t launch_both(const Geom& g, const TcPlan* pls, const BwdMaps& mkv, co
 
 template <int RANK>
 cudaError_t by_type(int dtype, const Geom& g, const TcPlan* pl, const BwdMaps& mkv, const BwdMaps& mq,
-                    float* rv, const float* lse, cudaStream_t st) {
+                    const void* o, const void* d_o, float* rv, const float* lse, cudaStream_t st) {
   const bool bf = dtype == 2;
   if (g.D == 64)
-    return bf ? launch_both<RANK, 64, true>(g, pl, mkv, mq, rv, lse, st)
-              : launch_both<RANK, 64, false>(g, pl, mkv, mq, rv, lse, st);
-  return bf ? launch_both<RANK, 32, true>(g, pl, mkv, mq, rv, lse, st)
-            : launch_both<RANK, 32, false>(g, pl, mkv, mq, rv, lse, st);
+    return bf ? launch_all<RANK, 64, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
+              : launch_all<RANK, 64, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+  return bf ? launch_all<RANK, 32, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
+            : launch_all<RANK, 32, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
 }
 
 }  // namespace
@@ -798,11 +920,6 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
                    float* Dvec, cudaStream_t st, int* launches) {
   const char* why;
   if (!tc_supported(dtype, g, &why)) return cudaErrorNotSupported;
-  // Row-vector layout: rank 1, written by the dQ kernel (fused preprocess;
-  // slots no token maps to, ragged residue classes, must read as 0);
-  // otherwise by the preprocess kernel.
-  cudaError_t e = g.rank == 1 ? rv_clear_padding(g, Dvec, st) : bwd_preprocess(dtype, g, o, d_o, lse, Dvec, st);
-  if (e != cudaSuccess) return e;
   // Each kernel has its own plan (na_tune may measure different winners).
   const PlanChoice pc = plan_choice(g, dtype);
   const TcPlan pls[2] = {make_plan(g, 128, pc.dkdv), make_plan(g, 128, pc.dq)};
@@ -812,6 +929,7 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   const void* tile_src[2][2] = {{k, v}, {q, d_o}};
   const void* chunk_src[2][2] = {{q, d_o}, {k, v}};
   BwdMaps* mm[2] = {&mkv, &mq};
+  cudaError_t e;
   for (int w = 0; w < 2; ++w) {
     const TcPlan& pl = pls[w];
     if ((e = make_map(&mm[w]->a0, dtype, g, tile_src[w][0], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
@@ -827,9 +945,9 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   mkv.o = mq.o;
   *launches = g.rank == 1 ? 2 : 3;
   switch (g.rank) {
-    case 1: return by_type<1>(dtype, g, pls, mkv, mq, Dvec, lse, st);
-    case 2: return by_type<2>(dtype, g, pls, mkv, mq, Dvec, lse, st);
-    default: return by_type<3>(dtype, g, pls, mkv, mq, Dvec, lse, st);
+    case 1: return by_type<1>(dtype, g, pls, mkv, mq, o, d_o, Dvec, lse, st);
+    case 2: return by_type<2>(dtype, g, pls, mkv, mq, o, d_o, Dvec, lse, st);
+    default: return by_type<3>(dtype, g, pls, mkv, mq, o, d_o, Dvec, lse, st);
   }
 }
 

@@ -275,7 +275,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (!t.init(g, pl, tile)) continue;
       RowCtx<RANK> r;
       r.init(g, pl, t, row);
-      float m_ref = -INFINITY, l = 0.f;
+      // l: sum of the fp32 probabilities (-> LSE); lr (bf16 only): sum of the
+      // values the PV MMA actually multiplies, bf16(P) -> O normalisation
+      // (R13).
+      float m_ref = -INFINITY, l = 0.f, lr = 0.f;
       int org[3] = {t.lo[0], t.lo[1], t.lo[2]};  // chunk origin (odometer)
       uint32_t mw[4];                             // this row's mask of the chunk
       r.chunk_mask(pl, org, mw);
@@ -345,12 +348,15 @@ __global__ void __launch_bounds__(kThreads, 2)
             NA_TMEM_ST16(trow + kColO + c0, ov);
           }
           l *= f;
+          if constexpr (BF16) lr *= f;
         } else if (need) {
           l = 0.f;  // no valid key seen yet on this row
+          lr = 0.f;
         }
         if (need) m_ref = mx2;
         const float nmu = m_ref == -INFINITY ? 0.f : -m_ref;
         float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        float2 accr0 = make_float2(0.f, 0.f), accr1 = make_float2(0.f, 0.f);
         // exponentials; P packed as 16-bit pairs IN PLACE: the pair of
         // columns (2i, 2i+1) goes to sv[i], whose logit was already consumed
 #pragma unroll
@@ -374,9 +380,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             acc1 = __fadd2_rn(acc1, p1);
             sv[16 * gq + (c >> 1)] = pack2<BF16>(p0.x, p0.y);
             sv[16 * gq + (c >> 1) + 1] = pack2<BF16>(p1.x, p1.y);
+            if constexpr (BF16) {
+              accr0 = __fadd2_rn(accr0, unpack2<BF16>(sv[16 * gq + (c >> 1)]));
+              accr1 = __fadd2_rn(accr1, unpack2<BF16>(sv[16 * gq + (c >> 1) + 1]));
+            }
           }
         }
         l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
+        if constexpr (BF16) lr += (accr0.x + accr0.y) + (accr1.x + accr1.y);
         if (tracer) NA_TRACE_EV(2, tr, 26);
         // P into its buffer once PV_{kv-1} has read the previous P
         if (kv > 0) ptx::mbar_wait(bar + B_PF, (kv - 1) & 1);
@@ -400,7 +411,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       ptx::mbar_wait(bar + B_OF, ti & 1);
       ptx::tc_fence_after();
       if (tracer) NA_TRACE_EV(2, tr, 22);
-      const float inv = l > 0.f ? 1.f / l : 0.f;
+      // bf16: O = sum bf16(P) v / sum bf16(P), a convex combination of the
+      // v's, so the 2^-9 rounding of P does not scale O (exact when one key
+      // dominates); fp16 P is 8x finer and uses l.
+      const float lo = BF16 ? lr : l;
+      const float inv = lo > 0.f ? 1.f / lo : 0.f;
       const int qb = ti & 1;
       uint8_t* stage = smem + S::kQ + qb * S::kTile;
 #pragma unroll
@@ -449,12 +464,8 @@ template <int RANK, int D, bool BF16>
 cudaError_t launch(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse, cudaStream_t st) {
   auto kern = fna_fwd_tc<RANK, D, BF16>;
   const int smem = FwdSmem<D>::kBytes + 1024;
-  static bool attr = false;  // benign race: idempotent
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
   const long long tiles = (long long)g.BH * pl.nres * pl.tiles;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const long long per = 2;  // CTAs per SM (TMEM: 256 columns each)

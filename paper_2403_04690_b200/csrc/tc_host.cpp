@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -262,7 +263,18 @@ void choice_key(const Geom& g, int dtype, int* key) {
 }
 }  // namespace
 
+namespace {
+thread_local bool g_override_on = false;
+thread_local PlanChoice g_override{0, 0, 0};
+}  // namespace
+
+void set_plan_override(const PlanChoice* c) {
+  g_override_on = c != nullptr;
+  if (c) g_override = *c;
+}
+
 PlanChoice plan_choice(const Geom& g, int dtype) {
+  if (g_override_on) return g_override;
   int key[16];
   choice_key(g, dtype, key);
   std::lock_guard<std::mutex> lk(g_choice_mu);
@@ -294,15 +306,39 @@ int tc_plan_candidates(const Geom& g) {
 }
 
 int num_sms() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-  if (!cache[dev]) {
-    int n = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (!n) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    cache[dev] = n > 0 ? n : 148;
+    n = n > 0 ? n : 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
-  return cache[dev];
+  return n;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device context: set it
+// once per (kernel, device), remembered in a small table (one process may
+// drive several GPUs).
+cudaError_t ensure_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, unsigned long long>> done;  // kernel -> device bitmask
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == func) {
+      if (d.second & bit) return cudaSuccess;
+      e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e == cudaSuccess) d.second |= bit;
+      return e;
+    }
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(func, bit);
+  return e;
 }
 
 namespace {
@@ -332,8 +368,10 @@ EncodeTiled encoder() {
 // dims (innermost first) = D, X_{R-1}, ..., X_0, BH.  The box is `box`
 // compacted tokens per axis (box_x on the innermost axis, per TMA issue),
 // walked with elementStrides = dilation so one box covers one residue class.
-cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base, const int box[3],
-                     int box_x) {
+namespace {
+
+cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* base, const int box[3],
+                       int box_x) {
   EncodeTiled enc = encoder();
   if (!enc) return cudaErrorNotSupported;
   const int R = g.rank;
@@ -361,6 +399,40 @@ cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* bas
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+// Encoded maps are cached per host thread, keyed by everything the encoding
+// reads (base pointer, dtype, geometry, box): a map holds only an address
+// and a geometry, so a hit is exactly the map encoding would produce, and a
+// steady-state call (same buffers) encodes nothing.
+cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base, const int box[3],
+                     int box_x) {
+  struct Entry {
+    int key[14];
+    const void* base;
+    CUtensorMap map;
+  };
+  constexpr int kEntries = 64;
+  thread_local Entry cache[kEntries];
+  thread_local int used = 0, next = 0;
+  const int key[14] = {dtype, g.rank, g.D, g.BH, box_x, g.L[0], g.L[1], g.L[2], g.dil[0], g.dil[1], g.dil[2],
+                       box[0], box[1], box[2]};
+  for (int i = 0; i < used; ++i)
+    if (cache[i].base == base && std::equal(key, key + 14, cache[i].key)) {
+      *map = cache[i].map;
+      return cudaSuccess;
+    }
+  const cudaError_t e = encode_map(map, dtype, g, base, box, box_x);
+  if (e != cudaSuccess) return e;
+  Entry& en = cache[next];
+  next = (next + 1) % kEntries;
+  if (used < kEntries) ++used;
+  std::copy(key, key + 14, en.key);
+  en.base = base;
+  en.map = *map;
+  return cudaSuccess;
 }
 
 }  // namespace na

@@ -132,8 +132,22 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(device):
+    """The current torch stream of `device` (the tensors' device, which the
+    caller has made current with torch.cuda.device)."""
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _need_lse(lse: torch.Tensor, q: torch.Tensor):
+    if lse.device != q.device or lse.dtype != torch.float32 or lse.shape != q.shape[:-1] or \
+            not lse.is_contiguous():
+        raise ValueError(f"lse must be a contiguous fp32 tensor of shape {tuple(q.shape[:-1])} "
+                         f"on {q.device}")
+
+
+def _need_cuda(q: torch.Tensor):
+    if q.device.type != "cuda":
+        raise ValueError("libna runs on CUDA tensors only (there is no CPU path)")
 
 
 def _need(t: torch.Tensor, like: torch.Tensor, name: str):
@@ -174,36 +188,47 @@ def profile_collect(max_entries: int = 4096):
 
 def na_fwd(q, k, v, kernel_size, dilation=None, is_causal=None, scale=None, impl="auto",
            out=None, lse=None, return_lse=True):
-    """Fused NA forward.  Returns (O, LSE) (LSE fp32 [B,H,X...]) or O."""
+    """Fused NA forward.  Returns (O, LSE) (LSE fp32 [B,H,X...]) or O.
+    Enqueued on the current stream of q's device."""
     p = _problem_from(q, kernel_size, dilation, is_causal, scale, impl)
+    _need_cuda(q)
     for t, n in ((q, "q"), (k, "k"), (v, "v")):
         _need(t, q, n)
-    o = torch.empty_like(q) if out is None else out
-    _need(o, q, "out")
-    if return_lse and lse is None:
-        lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
-    _check(lib().na_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
-                        _ptr(lse) if return_lse else None, _stream()))
+    with torch.cuda.device(q.device):
+        o = torch.empty_like(q) if out is None else out
+        _need(o, q, "out")
+        if return_lse:
+            if lse is None:
+                lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
+            _need_lse(lse, q)
+        _check(lib().na_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                            _ptr(lse) if return_lse else None, _stream(q.device)))
     return (o, lse) if return_lse else o
 
 
 def na_bwd(q, k, v, o, d_o, lse, kernel_size, dilation=None, is_causal=None, scale=None,
            impl="auto", dq=None, dk=None, dv=None, workspace=None):
-    """Fused NA backward.  Returns (dQ, dK, dV)."""
+    """Fused NA backward.  Returns (dQ, dK, dV).  Enqueued on the current
+    stream of q's device."""
     p = _problem_from(q, kernel_size, dilation, is_causal, scale, impl)
+    _need_cuda(q)
     for t, n in ((k, "k"), (v, "v"), (o, "o"), (d_o, "d_o")):
         _need(t, q, n)
-    if lse.dtype != torch.float32 or lse.shape != q.shape[:-1] or not lse.is_contiguous():
-        raise ValueError("lse must be a contiguous fp32 [B, H, X...] tensor")
-    dq = torch.empty_like(q) if dq is None else dq
-    dk = torch.empty_like(q) if dk is None else dk
-    dv = torch.empty_like(q) if dv is None else dv
-    need = na_bwd_workspace_size(p)
-    if workspace is None:
-        workspace = torch.empty((max(need, 16) + 3) // 4, dtype=torch.float32, device=q.device)
-    _check(lib().na_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(d_o), _ptr(lse),
-                        _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace),
-                        workspace.numel() * workspace.element_size(), _stream()))
+    _need_lse(lse, q)
+    with torch.cuda.device(q.device):
+        dq = torch.empty_like(q) if dq is None else dq
+        dk = torch.empty_like(q) if dk is None else dk
+        dv = torch.empty_like(q) if dv is None else dv
+        for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+            _need(t, q, n)
+        need = na_bwd_workspace_size(p)
+        if workspace is None:
+            workspace = torch.empty((max(need, 16) + 3) // 4, dtype=torch.float32, device=q.device)
+        if workspace.device != q.device or not workspace.is_contiguous():
+            raise ValueError(f"workspace must be a contiguous tensor on {q.device}")
+        _check(lib().na_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(d_o),
+                            _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace),
+                            workspace.numel() * workspace.element_size(), _stream(q.device)))
     return dq, dk, dv
 
 
@@ -227,12 +252,15 @@ def na_tune(q, k, v, d_o, kernel_size, dilation=None, is_causal=None, scale=None
     dK/dV and dQ separately) on scratch outputs and keep the fastest for later
     calls with the same geometry.  Returns the picks (fwd, dkdv, dq)."""
     p = _problem_from(q, kernel_size, dilation, is_causal, scale, "auto")
+    _need_cuda(q)
     for t, n in ((k, "k"), (v, "v"), (d_o, "d_o")):
         _need(t, q, n)
     o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
     lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
     ws = torch.empty((max(na_bwd_workspace_size(p), 16) + 3) // 4, dtype=torch.float32, device=q.device)
     c = (ctypes.c_int32 * 3)()
-    _check(lib().na_tune(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(d_o),
-                         _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel() * 4, _stream(), c))
+    with torch.cuda.device(q.device):
+        _check(lib().na_tune(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                             _ptr(d_o), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel() * 4,
+                             _stream(q.device), c))
     return tuple(c)

@@ -372,6 +372,37 @@ def test_token_forms_equal_full_forms(case):
     np.testing.assert_allclose(lse.reshape(-1), lt, rtol=0, atol=1e-13)
 
 
+@pytest.mark.parametrize("stored", [False, True])
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("case", CASES)
+def test_gather_and_token_forms_equal_scatter_form_16bit(case, dt, stored):
+    """The per-token (bwd_tokens) and whole-problem gather (bwd_gather) forms
+    of the backward equal the scatter form (bwd) on 16-bit inputs, with the
+    exact D_x and with the stored-O D_x of reading R12 -- the scatter form
+    with stored_o is itself pinned to torch's dense formula above
+    (test_stored_output_backward_matches_dense_formula), so every form the
+    GPU parity tests use is pinned."""
+    extent, kernel, dil, causal = case
+    D, B, H = 8, 1, 2
+    q, k, v, do = (t.to(dt) for t in problem_inputs(extent, D, B, H, seed=101, with_do=True))
+    p = oracle.make_problem(B, H, extent, D, kernel, dil, causal)
+    full = oracle.bwd(p, q, k, v, do, stored_o=stored)
+    N = int(np.prod(extent))
+    toks = np.arange(B * H * N)
+    tok = oracle.bwd_tokens(p, q, k, v, do, toks, stored_o=stored)
+    gat = oracle.bwd_gather(p, q, k, v, do, stored_o=stored)
+    for f, t, g in zip(full, tok, gat):
+        np.testing.assert_allclose(f.reshape(-1, D), t, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(f, g, rtol=0, atol=1e-12)
+    o, lse = oracle.fwd(p, q, k, v)
+    of, lf = oracle.fwd_full_tokens(p, q, k, v)
+    np.testing.assert_allclose(o, of, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(lse, lf, rtol=0, atol=1e-13)
+    if stored:  # the stored-O term is not a no-op on these inputs
+        exact = oracle.bwd(p, q, k, v, do, stored_o=False)
+        assert np.abs(exact[0] - full[0]).max() > 0
+
+
 def test_half_inputs_are_upcast_exactly():
     """fp16 / bf16 inputs give the same result as their exact fp64 upcast."""
     q, k, v = problem_inputs([9], 8, seed=110)
