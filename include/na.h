@@ -74,8 +74,13 @@ typedef enum {
 } na_status;
 
 /* Kernel family selection (tests and benchmarks use it to pin a path). */
+/* Kernel family selection.  There is no silent fallback: with NA_IMPL_AUTO a
+ * 16-bit problem runs on the tensor cores, and a 16-bit problem outside that
+ * path (tc_supported: head_dim or dilation limits) fails with NA_ERR_IMPL
+ * unless the caller selects NA_IMPL_SIMT explicitly.  fp32 inputs always run
+ * on the CUDA-core kernels (TF32 off, north_star's 1e-4 bound). */
 typedef enum {
-  NA_IMPL_AUTO = 0,  /* tensor-core path when the problem fits it, else SIMT  */
+  NA_IMPL_AUTO = 0,  /* fp16/bf16: tensor cores (or NA_ERR_IMPL); fp32: SIMT */
   NA_IMPL_SIMT = 1,  /* fp32 CUDA-core kernels (any dtype; fp32 inputs always) */
   NA_IMPL_TC = 2     /* tcgen05 + TMEM + TMA kernels (fp16 / bf16 only)        */
 } na_impl;
@@ -111,12 +116,19 @@ size_t na_bwd_workspace_size(const na_problem* p);
 
 /* Backward.  Reads q, k, v, o, d_o (dL/dO) and lse from na_fwd on the same
  * inputs; writes dq, dk, dv (each element by exactly one thread; no
- * atomics).  The softmax-Jacobian term D_x = <dO_x, O_x> is formed from the
- * `o` passed in, i.e. the stored (dtype-rounded) forward output (DESIGN.md
- * reading R12).  `workspace` (device, >= na_bwd_workspace_size bytes) is
- * scratch owned by the caller.  Three launches on `stream`:
- * D_x = <dO_x, O_x>, then dK/dV (key-stationary, inverse neighborhood map),
- * then dQ (query-stationary, forward map). */
+ * atomics).  The softmax-Jacobian term D_x = sum_y P_xy dP_xy = <dO_x, O_x>
+ * (reading R12): fp16 forms it from the `o` passed in (the stored
+ * forward output); bf16, whose stored O is 8x coarser, uses <dO_x, o_x> only
+ * as an estimate and corrects it inside the dQ kernel to sum_y P_xy dP_xy in
+ * fp32, so its gradient is that of the exact forward.  `workspace` (device,
+ * >= na_bwd_workspace_size bytes) is scratch owned by the caller.  Launches
+ * on `stream`, in order:
+ *   rank 1:   [a memset of the workspace's padding slots when a residue
+ *             class is ragged], dQ (query-stationary, forward map; it also
+ *             forms the row values -LSE_x*log2(e), D_x from the O and dO
+ *             tiles it loads), then dK/dV (key-stationary, inverse map);
+ *   rank 2-3: the row-value pass (-LSE_x*log2(e), <dO_x, O_x>), dQ, dK/dV.
+ * na_last_launch_count() reports the number of kernels (2 or 3). */
 na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* v,
                  const void* o, const void* d_o, const float* lse, void* dq, void* dk,
                  void* dv, void* workspace, size_t workspace_bytes, void* stream);
@@ -142,7 +154,8 @@ na_status na_get_plan_choice(const na_problem* p, int32_t choice[3]);
 na_status na_set_plan_choice(const na_problem* p, const int32_t choice[3]);
 
 /* Which kernel family na_fwd/na_bwd would run for `p` (NA_IMPL_SIMT or
- * NA_IMPL_TC), or -1 if `p` is invalid.  Host only. */
+ * NA_IMPL_TC), or -1 if `p` is invalid or its `impl` cannot run it (the calls
+ * would return NA_ERR_IMPL).  Host only. */
 int na_selected_impl(const na_problem* p);
 
 /* Static description of a status code. */

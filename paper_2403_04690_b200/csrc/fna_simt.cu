@@ -11,6 +11,7 @@
 //   fna_dq_simt     : dQ_x = scale sum_y P(dP - D_x) k_y     (NN on dA)
 //   fna_dkdv_simt   : dK_y, dV_y over the inverse window     (IN)
 #include <cuda_bf16.h>
+#include <type_traits>
 #include <cuda_fp16.h>
 
 #include "na_geom.cuh"
@@ -237,20 +238,27 @@ __global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__
                                                    const T* __restrict__ v,
                                                    const T* __restrict__ d_o,
                                                    const float* __restrict__ lse,
-                                                   const float* __restrict__ Dvec,
+                                                   float* __restrict__ Dvec,
                                                    T* __restrict__ dq) {
+  // 16-bit inputs: D_x read from Dvec is <dO_x, O_x> with the stored
+  // (rounded) O, an estimate; c = sum_y P_xy (dP_xy - Dt_x) = D_x - Dt_x and
+  // PK = sum_y P_xy k_y are accumulated alongside, dQ = scale (acc - c PK) is
+  // the gradient with D_x = sum_y P_xy dP_xy, and Dt_x + c is written back
+  // for the dK/dV kernel, which runs after this one (R12).
+  constexpr bool kCorr = !std::is_same<T, float>::value;
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   const int bh = (int)(row / g.N), x = (int)(row % g.N);
   const int64_t base = (int64_t)bh * g.N * g.D;
-  float qr[DPL], dor[DPL], acc[DPL];
+  float qr[DPL], dor[DPL], acc[DPL], pk[DPL];
+  float csum = 0.f;
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
     int d = lane + 32 * i;
     qr[i] = d < g.D ? ld(q + base + (int64_t)x * g.D + d) : 0.f;
     dor[i] = d < g.D ? ld(d_o + base + (int64_t)x * g.D + d) : 0.f;
-    acc[i] = 0.f;
+    acc[i] = pk[i] = 0.f;
   }
   const float lse_x = lse[row], D_x = Dvec[row];
   const Coord co = decode(g, x);
@@ -278,17 +286,23 @@ __global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__
         dp = warp_sum(dp);
         const float p = __expf(s * g.scale - lse_x);
         const float ds = p * (dp - D_x);
+        if constexpr (kCorr) csum += ds;
 #pragma unroll
         for (int i = 0; i < DPL; ++i) {
           int d = lane + 32 * i;
-          if (d < g.D) acc[i] = fmaf(ds, ld(k + y + d), acc[i]);
+          if (d < g.D) {
+            const float kv = ld(k + y + d);
+            acc[i] = fmaf(ds, kv, acc[i]);
+            if constexpr (kCorr) pk[i] = fmaf(p, kv, pk[i]);
+          }
         }
       }
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
     int d = lane + 32 * i;
-    if (d < g.D) dq[base + (int64_t)x * g.D + d] = cvt<T>(acc[i] * g.scale);
+    if (d < g.D) dq[base + (int64_t)x * g.D + d] = cvt<T>((acc[i] - csum * pk[i]) * g.scale);
   }
+  if (kCorr && lane == 0) Dvec[row] = D_x + csum;
 }
 
 // ------------------------------------------------------------- bwd: dK, dV
@@ -379,13 +393,14 @@ cudaError_t launch_bwd(const Geom& g, const void* q, const void* k, const void* 
   prof_begin(KID_BWD_PRE, st);
   fna_bwd_pre<T><<<grid, 256, 0, st>>>(g, (const T*)o, (const T*)d_o, Dvec);
   prof_end(st);
-  prof_begin(KID_DKDV_SIMT, st);
-  fna_dkdv_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
-                                              (const T*)d_o, lse, Dvec, (T*)dk, (T*)dv);
-  prof_end(st);
+  // dQ first: for 16-bit inputs it corrects D_x in Dvec for dK/dV
   prof_begin(KID_DQ_SIMT, st);
   fna_dq_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
                                             (const T*)d_o, lse, Dvec, (T*)dq);
+  prof_end(st);
+  prof_begin(KID_DKDV_SIMT, st);
+  fna_dkdv_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
+                                              (const T*)d_o, lse, Dvec, (T*)dk, (T*)dv);
   prof_end(st);
   return cudaGetLastError();
 }

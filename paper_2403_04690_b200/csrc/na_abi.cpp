@@ -125,16 +125,21 @@ size_t bwd_workspace_bytes(const na::Geom& g) {
   return simt > tc ? simt : tc;
 }
 
-// Which family runs problem p (assumes p validated).
+// Which family runs problem p (assumes p validated), or -1: no silent
+// fallback -- a 16-bit problem runs on the tensor cores unless the caller
+// asks for the CUDA-core kernels explicitly (NA_IMPL_SIMT).
 int select_impl(const na_problem* p, const na::Geom& g, const char** why) {
   *why = "";
   if (p->dtype == NA_F32) {
-    *why = "fp32 runs on CUDA cores (TF32 off)";
+    if (p->impl == NA_IMPL_TC) {
+      *why = "fp32 inputs run on the CUDA-core kernels (TF32 off)";
+      return -1;
+    }
     return NA_IMPL_SIMT;
   }
   if (p->impl == NA_IMPL_SIMT) return NA_IMPL_SIMT;
   if (na::tc_supported((int)p->dtype, g, why)) return NA_IMPL_TC;
-  return NA_IMPL_SIMT;
+  return -1;
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
@@ -216,8 +221,9 @@ na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* 
   na::Geom g = make_geom(p);
   const char* why;
   int impl = select_impl(p, g, &why);
-  if (p->impl == NA_IMPL_TC && impl != NA_IMPL_TC)
-    return fail(NA_ERR_IMPL, "tensor-core path cannot run this problem: %s", why);
+  if (impl < 0)
+    return fail(NA_ERR_IMPL, "tensor-core path cannot run this problem: %s (impl=NA_IMPL_SIMT selects the "
+                "CUDA-core kernels explicitly)", why);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int launches = 1;
   cudaError_t e = impl == NA_IMPL_TC ? na::tc_fwd((int)p->dtype, g, q, k, v, o, lse, st, &launches)
@@ -252,8 +258,9 @@ na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* 
                 workspace_bytes);
   const char* why;
   int impl = select_impl(p, g, &why);
-  if (p->impl == NA_IMPL_TC && impl != NA_IMPL_TC)
-    return fail(NA_ERR_IMPL, "tensor-core path cannot run this problem: %s", why);
+  if (impl < 0)
+    return fail(NA_ERR_IMPL, "tensor-core path cannot run this problem: %s (impl=NA_IMPL_SIMT selects the "
+                "CUDA-core kernels explicitly)", why);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int launches = 3;
   cudaError_t e =

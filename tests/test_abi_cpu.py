@@ -103,7 +103,21 @@ def test_workspace_size(na):
 
 def test_fp32_selects_simt(na):
     assert na.na_selected_impl(P(na, dtype=torch.float32)) == na.NA_IMPL_SIMT
+    assert na.na_selected_impl(P(na, dtype=torch.float32, impl="tc")) == -1
     assert na.na_selected_impl(P(na, kernel_size=[4])) == -1
+
+
+def test_no_silent_fallback_for_16bit(na):
+    """A 16-bit problem the tensor-core path cannot run is refused under AUTO
+    (NA_ERR_IMPL before any launch) and runs on the CUDA cores only when asked."""
+    L = na.lib()
+    p = P(na, extent=[200], kernel_size=[3], dilation=[9])  # dilation > 8: outside TMA strides
+    assert na.na_selected_impl(p) == -1
+    assert L.na_fwd(ctypes.byref(p), 16, 16, 16, 16, None, None) == 14  # NA_ERR_IMPL
+    assert b"NA_IMPL_SIMT" in L.na_last_error()
+    p = P(na, extent=[200], kernel_size=[3], dilation=[9], impl="simt")
+    assert na.na_selected_impl(p) == na.NA_IMPL_SIMT
+    assert na.na_selected_impl(P(na)) == na.NA_IMPL_TC
 
 
 def test_fwd_rejects_before_launch(na):
