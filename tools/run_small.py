@@ -12,6 +12,9 @@ cases = [
     ([300], [33], [2], [1], 64, torch.float16),
     ([20, 27], [7, 5], [2, 1], [0, 0], 32, torch.bfloat16),
     ([6, 10, 12], [3, 5, 5], [1, 1, 2], [1, 0, 0], 64, torch.float16),
+    ([300], [33], [2], [1], 64, torch.bfloat16),
+    ([20, 27], [7, 5], [2, 1], [0, 0], 64, torch.float16),
+    ([6, 10, 12], [3, 5, 5], [1, 1, 2], [1, 0, 0], 32, torch.bfloat16),
     ([50], [7], [1], [0], 16, torch.float32),
 ]
 for ext, ker, dil, cau, d, dt in cases:
