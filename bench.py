@@ -513,6 +513,49 @@ def per_config_table(args, world, rank, peaks):
     return out
 
 
+def cp_table(args, world, rank, peaks):
+    """Context parallelism (paper_2403_04690_b200/cp.py)
+    at N > 1: config B_d1 with ALL its B*H slices on every rank and the
+    sequence split over the ranks (owned rows + a halo of k*dil rows,
+    exchanged with NCCL send/recv).  fwd and fwd+bwd ms include the halo
+    exchanges; max over ranks."""
+    import paper_2403_04690_b200 as na
+    from paper_2403_04690_b200.cp import ContextParallel
+    cfg = na_synth.CONFIGS["B_d1"]
+    kw = dict(kernel_size=list(cfg.kernel_size), dilation=list(cfg.dilation),
+              is_causal=[bool(c) for c in cfg.is_causal])
+    cp = ContextParallel(list(cfg.extent), **kw)
+    a, b = cp.split.own(rank)
+    s0, e0 = cp.split.slab(rank)
+    q, k, v, do = (t.view(cfg.shape())[:, :, a:b].contiguous()
+                   for t in na_synth.make_inputs(cfg, device="cuda"))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    state = {}
+
+    def fwd():
+        state["o"], state["lse"], state["ctx"] = cp.forward(q, k, v)
+
+    def fwd_bwd():
+        fwd()
+        cp.backward(state["ctx"], do)
+
+    for _ in range(2):
+        fwd_bwd()
+    torch.cuda.synchronize()
+    barrier(world)
+    n_it = max(3, min(args.steps, 10))
+    f_ms = reduce_max(statistics.median(timed_steps(fwd, n_it, flush)), world)
+    fb_ms = reduce_max(statistics.median(timed_steps(fwd_bwd, n_it, flush)), world)
+    fl_fb = flops(cfg)
+    peak_tf = float(peaks.get("bf16_tflops", 1590.0))
+    return {"config": "B_d1", "split": f"axis 0 (L={cfg.extent[0]}) over {world} ranks",
+            "halo_rows": cp.split.halo, "slab_rows_rank0": list(cp.split.slab(0)),
+            "recompute_overhead": round((e0 - s0) / (b - a) - 1.0, 4),
+            "fwd_ms": round(f_ms, 4), "fwd_bwd_ms": round(fb_ms, 4),
+            "fwd_bwd_tflops": round(fl_fb / (fb_ms * 1e-3) / 1e12, 3),
+            "fwd_bwd_tensor_peak_frac": round(fl_fb / (fb_ms * 1e-3) / 1e12 / (world * peak_tf), 5)}
+
+
 def run_native(args, world, rank, local):
     na_peaks, peak_src = load_peaks()
     R = Runner(rank, world)
@@ -612,6 +655,13 @@ def run_native(args, world, rank, local):
     if not args.no_per_config:
         per_config = per_config_table(args, world, rank, na_peaks)
 
+    cp_res = None
+    if world > 1 and not args.no_per_config:
+        try:  # optional report item: never lose the bench line over it
+            cp_res = cp_table(args, world, rank, na_peaks)
+        except Exception as ex:  # pragma: no cover
+            cp_res = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -641,6 +691,7 @@ def run_native(args, world, rank, local):
                      "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src,
                      "step_share": shares, "kernels": per_kernel_roof},
         "per_config": per_config,
+        "context_parallel": cp_res,
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,

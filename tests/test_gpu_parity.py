@@ -354,3 +354,44 @@ def test_random_problems_match_oracle(na, ext, ker, dil, cau, D, dt):
         assert excess(dk.reshape(shp), rdk, dt) <= 0, pick
         assert excess(dv.reshape(shp), rdv, dt) <= 0, pick
     na.na_set_plan_choice(p, (0, 0, 0))
+
+
+# ------------------------------------------------------- context parallelism
+
+CP_CASES = [
+    ([4096], [255], [1], [0], 64, torch.float16, 4),
+    ([2000], [63], [4], [1], 64, torch.bfloat16, 3),
+    ([56, 40], [7, 7], [8, 1], [0, 0], 32, torch.float16, 2),
+    ([16, 24, 20], [7, 5, 5], [1, 1, 1], [1, 0, 0], 64, torch.float16, 4),
+]
+
+
+@pytest.mark.parametrize("ext,ker,dil,cau,D,dt,world", CP_CASES)
+def test_context_parallel_slabs_match_oracle(na, ext, ker, dil, cau, D, dt, world):
+    """SURVEY 8(f) rank 3 on the GPU kernels: every virtual rank's slab
+    (owned rows of axis 0 plus a halo of k_0*dil_0, paper_2403_04690_b200/cp.py)
+    is run through na_fwd / na_bwd as its own problem; the owned rows of O,
+    LSE, dQ, dK, dV, concatenated, match the oracle's exact whole-problem
+    result.  (The halo exchange itself is covered on CPU, tests/test_cp_cpu.py.)"""
+    from paper_2403_04690_b200.cp import make_split, slab_of
+    cfg = na_synth.small_config(ext, ker, dil, cau, head_dim=D, batch=1, heads=2, dtype=dt)
+    q, k, v, do = na_synth.make_inputs(cfg, salt=21)
+    split = make_split(ext, ker, dil, world)
+    kw = dict(kernel_size=ker, dilation=dil, is_causal=[bool(c) for c in cau])
+    parts = {n: [] for n in ("o", "lse", "dq", "dk", "dv")}
+    for g in range(world):
+        qs, ks, vs, dos = (slab_of(t, split, g).cuda() for t in (q, k, v, do))
+        o, lse = na.na_fwd(qs, ks, vs, **kw)
+        dq, dk, dv = na.na_bwd(qs, ks, vs, o, dos, lse, **kw)
+        a, b = split.own(g)
+        s0 = split.slab(g)[0]
+        for n, t in zip(parts, (o, lse, dq, dk, dv)):
+            parts[n].append(t[:, :, a - s0:b - s0].float().cpu())
+    op = oracle_problem(cfg)
+    ro, rlse = oracle.fwd(op, q, k, v)
+    rdq, rdk, rdv = oracle.bwd(op, q, k, v, do)
+    shp = tuple(q.shape)
+    for n, ref in (("o", ro), ("dq", rdq), ("dk", rdk), ("dv", rdv)):
+        got = torch.cat(parts[n], dim=2).numpy()
+        assert excess(got, ref.reshape(shp), dt) <= 0, (n, max_err(got, ref.reshape(shp)))
+    assert max_err(torch.cat(parts["lse"], dim=2).numpy(), rlse.reshape(shp[:-1])) <= LSE_TOL[dt]
