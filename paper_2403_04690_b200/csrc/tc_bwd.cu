@@ -293,7 +293,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     // its own issuing thread: B_S (S warp); B_PE, B_E, B_OF (OUT warp) -- the
     // S/dP MMAs of a chunk are complete before its last OUT is issued (the
     // warpgroup read their results first), so B_E covers both.
-    constexpr uint32_t kSw = D == 64 ? 2u : 4u;
+    constexpr uint32_t kSw = ptx::sw_layout(D);
     constexpr uint32_t kSbo = 8 * S::kRowBytes;
     int tr = 0;
     (void)tr;
@@ -502,7 +502,20 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + q, S::kRowBytes)) =
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
       }
-      if (c0 < ncols) {  // a 16-column remainder (dQ halves at D = 32)
+      if (c0 + 8 == ncols) {  // an 8-column remainder (dQ halves at D = 16)
+        uint32_t ov[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3]), "=r"(ov[4]), "=r"(ov[5]),
+                       "=r"(ov[6]), "=r"(ov[7])
+                     : "r"(trow + src + c0));
+        ptx::tmem_ld_wait();
+        uint32_t pk[4];
+#pragma unroll
+        for (int c = 0; c < 8; c += 2)
+          pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
+        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, (col0 + c0) / 8, S::kRowBytes)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      } else if (c0 < ncols) {  // a 16-column remainder (dQ halves at D = 32)
         uint32_t ov[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -525,6 +538,26 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     // Exact-D dQ drain: (dQacc - c_x PK_x) * scale, 16 columns per round trip.
     auto drain_exact = [&](uint32_t src, uint32_t src_pk, uint8_t* stage, int col0, int ncols, float mul,
                            float corr) {
+      if (ncols == 8) {  // D = 16: each group drains 8 columns
+        uint32_t ov[8], kv_[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3]), "=r"(ov[4]), "=r"(ov[5]),
+                       "=r"(ov[6]), "=r"(ov[7])
+                     : "r"(trow + src));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(kv_[0]), "=r"(kv_[1]), "=r"(kv_[2]), "=r"(kv_[3]), "=r"(kv_[4]), "=r"(kv_[5]),
+                       "=r"(kv_[6]), "=r"(kv_[7])
+                     : "r"(trow + src_pk));
+        ptx::tmem_ld_wait();
+        uint32_t pk[4];
+#pragma unroll
+        for (int c = 0; c < 8; c += 2)
+          pk[c >> 1] = pack2<BF16>((__uint_as_float(ov[c]) - corr * __uint_as_float(kv_[c])) * mul,
+                                   (__uint_as_float(ov[c + 1]) - corr * __uint_as_float(kv_[c + 1])) * mul);
+        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, col0 / 8, S::kRowBytes)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        return;
+      }
       for (int c0 = 0; c0 < ncols; c0 += 16) {
         uint32_t ov[16], kv_[16];
         NA_TMEM_LD16(trow + src + c0, ov);
@@ -909,6 +942,9 @@ cudaError_t by_type(int dtype, const Geom& g, const TcPlan* pl, const BwdMaps& m
   if (g.D == 64)
     return bf ? launch_all<RANK, 64, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
               : launch_all<RANK, 64, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+  if (g.D == 16)
+    return bf ? launch_all<RANK, 16, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
+              : launch_all<RANK, 16, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
   return bf ? launch_all<RANK, 32, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
             : launch_all<RANK, 32, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
 }

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     // Issue order S_0, [SF_0] S_1, [P_0] PV_0, [SF_1] S_2, [P_1] PV_1, ...:
     // S_{kv+1} starts as soon as the softmax warps have LOADED S_kv, so it
     // overlaps their exponentials; PV_kv reads P from its own buffer.
-    constexpr uint32_t kSw = D == 64 ? 2u : 4u;  // SW128 : SW64
+    constexpr uint32_t kSw = ptx::sw_layout(D);  // SW128 / SW64 / SW32
     constexpr uint32_t kSbo = 8 * S::kRowBytes;  // 8-row core-matrix group
     const uint32_t idesc_s = ptx::make_idesc(128, pl.n_kv, BF16, false);
     constexpr uint32_t idesc_o = ptx::make_idesc(128, D, BF16, true);
@@ -419,12 +419,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int qb = ti & 1;
       uint8_t* stage = smem + S::kQ + qb * S::kTile;
 #pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t ov[32];
-        NA_TMEM_LD32(trow + kColO + c0, ov);
+      constexpr int kEc = D < 32 ? 16 : 32;  // O columns per TMEM load
+      for (int c0 = 0; c0 < D; c0 += kEc) {
+        uint32_t ov[kEc];
+        if constexpr (kEc == 32) NA_TMEM_LD32(trow + kColO + c0, ov);
+        else NA_TMEM_LD16(trow + kColO + c0, ov);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 32; c += 8)
+        for (int c = 0; c < kEc; c += 8)
           *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, (c0 + c) / 8, S::kRowBytes)) =
               make_uint4(pack2<BF16>(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv),
                          pack2<BF16>(__uint_as_float(ov[c + 2]) * inv, __uint_as_float(ov[c + 3]) * inv),
@@ -482,6 +484,8 @@ cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const FwdMaps& m
   const bool bf = dtype == 2;
   if (g.D == 64) return bf ? launch<RANK, 64, true>(g, pl, maps, lse, st)
                            : launch<RANK, 64, false>(g, pl, maps, lse, st);
+  if (g.D == 16) return bf ? launch<RANK, 16, true>(g, pl, maps, lse, st)
+                           : launch<RANK, 16, false>(g, pl, maps, lse, st);
   return bf ? launch<RANK, 32, true>(g, pl, maps, lse, st) : launch<RANK, 32, false>(g, pl, maps, lse, st);
 }
 

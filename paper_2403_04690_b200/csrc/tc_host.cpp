@@ -20,7 +20,7 @@ namespace na {
 
 bool tc_supported(int dtype, const Geom& g, const char** why) {
   if (dtype != 1 && dtype != 2) { *why = "tensor-core path is fp16/bf16 only"; return false; }
-  if (g.D != 32 && g.D != 64) { *why = "tensor-core path needs head_dim 32 or 64"; return false; }
+  if (g.D != 16 && g.D != 32 && g.D != 64) { *why = "tensor-core path needs head_dim 16, 32 or 64"; return false; }
   for (int a = 0; a < g.rank; ++a) {
     if (g.dil[a] > 8) { *why = "TMA element strides limit dilation to <= 8"; return false; }
   }
@@ -393,7 +393,9 @@ cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* b
   strides[R] = row * g.N;
   boxd[R + 1] = 1;
   estr[R + 1] = 1;
-  const CUtensorMapSwizzle sw = g.D == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const CUtensorMapSwizzle sw = g.D == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                               : g.D == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_32B;
   CUresult r = enc(map, dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    R + 2, const_cast<void*>(base), dims, strides, boxd, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -172,12 +172,17 @@ __device__ __forceinline__ void bulk_wait() {
 }
 
 // Byte offset of 16-byte chunk `chunk` of row `row` in a TMA box whose rows
-// are `row_bytes` (128 or 64) long with the matching hardware swizzle
-// (SWIZZLE_128B: chunk ^ (row % 8); SWIZZLE_64B: chunk ^ ((row / 2) % 4)).
+// are `row_bytes` (128, 64 or 32) long with the matching hardware swizzle
+// (SWIZZLE_128B: chunk ^ (row % 8); SWIZZLE_64B: chunk ^ ((row / 2) % 4);
+// SWIZZLE_32B: chunk ^ ((row / 4) % 2) -- address bits [4, 4+b) ^= [7, 7+b)).
 __device__ __forceinline__ uint32_t swz_off(uint32_t row, uint32_t chunk, uint32_t row_bytes) {
   return row_bytes == 128 ? row * 128 + ((chunk ^ (row & 7)) << 4)
-                          : row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
+         : row_bytes == 64 ? row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4)
+                           : row * 32 + ((chunk ^ ((row >> 2) & 1)) << 4);
 }
+// Shared-memory descriptor layout code of the swizzle a D-wide 16-bit row uses
+// (2 = SW128, 4 = SW64, 6 = SW32).
+__host__ __device__ constexpr uint32_t sw_layout(int D) { return D == 64 ? 2u : D == 32 ? 4u : 6u; }
 
 // ------------------------------------------------------------------- tcgen05
 template <int NCOLS>
