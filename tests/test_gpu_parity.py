@@ -70,7 +70,7 @@ SMALL = [
 
 
 def small_cases():
-    for (ext, ker, dil, cau), D, dt in itertools.product(SMALL, [32, 64],
+    for (ext, ker, dil, cau), D, dt in itertools.product(SMALL, [16, 32, 64],
                                                           [torch.float16, torch.bfloat16]):
         yield pytest.param(ext, ker, dil, cau, D, dt, id=f"{ext}-k{ker}-d{dil}-c{cau}-D{D}-{str(dt)[6:]}")
     for ext, ker, dil, cau in SMALL[::3]:
@@ -325,7 +325,7 @@ def _random_cases(n=24, seed=2024):
             if k < 1:
                 k = 1
             ext.append(L), ker.append(k), dil.append(d), cau.append(c)
-        D = int(rng.choice([32, 64]))
+        D = int(rng.choice([16, 32, 64]))
         dt = [torch.float16, torch.bfloat16][int(rng.integers(0, 2))]
         out.append((ext, ker, dil, cau, D, dt))
     return out
