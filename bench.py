@@ -430,6 +430,8 @@ def per_config_table(args, world, rank, peaks):
             dq, dk, dv = (torch.empty_like(q) for _ in range(3))
             pr = na.make_problem(1, n, list(cfg.extent), cfg.head_dim, **kw, dtype=cfg.dtype)
             impl = {na.NA_IMPL_TC: "tc", na.NA_IMPL_SIMT: "simt"}.get(na.na_selected_impl(pr))
+            if cfg.dtype == torch.bfloat16 and impl == "tc":  # DESIGN.md R13 variant
+                impl += "-bf16-precise" if na.na_bf16_precise(pr) == 1 else "-bf16-plain"
             ws = torch.empty((na.na_bwd_workspace_size(pr) + 3) // 4, dtype=torch.float32, device="cuda")
 
             def fwd():

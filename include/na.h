@@ -118,9 +118,10 @@ size_t na_bwd_workspace_size(const na_problem* p);
  * inputs; writes dq, dk, dv (each element by exactly one thread; no
  * atomics).  The softmax-Jacobian term D_x = sum_y P_xy dP_xy = <dO_x, O_x>
  * (reading R12): fp16 forms it from the `o` passed in (the stored
- * forward output); bf16, whose stored O is 8x coarser, uses <dO_x, o_x> only
- * as an estimate and corrects it inside the dQ kernel to sum_y P_xy dP_xy in
- * fp32, so its gradient is that of the exact forward.  `workspace` (device,
+ * forward output); bf16 in its precise variant (na_bf16_precise), whose
+ * stored O is 8x coarser, uses <dO_x, o_x> only as an estimate and corrects
+ * it inside the dQ kernel to sum_y P_xy dP_xy in fp32, so its gradient is
+ * that of the exact forward.  `workspace` (device,
  * >= na_bwd_workspace_size bytes) is scratch owned by the caller.  Launches
  * on `stream`, in order:
  *   rank 1:   [a memset of the workspace's padding slots when a residue
@@ -157,6 +158,17 @@ na_status na_set_plan_choice(const na_problem* p, const int32_t choice[3]);
  * NA_IMPL_TC), or -1 if `p` is invalid or its `impl` cannot run it (the calls
  * would return NA_ERR_IMPL).  Host only. */
 int na_selected_impl(const na_problem* p);
+
+/* bf16 on the tensor cores (R13): 1 if na_fwd / na_bwd run the
+ * error-compensated variant for `p` (O normalised by the sum of the
+ * bf16-rounded P; the backward's bf16 P / dS MMA operands split hi + lo and
+ * D_x corrected in the dQ kernel), 0 if the plain one (also for every
+ * non-bf16 or non-tensor-core problem), -1 if `p` is invalid.  The precise
+ * variant runs when some window holds fewer than 128 keys -- the product of
+ * k over the NON-causal axes (a causal axis leaves its first query a single
+ * key) -- where single probabilities approach 1 and outputs reach magnitudes
+ * whose bf16 half-ulp leaves too little of the 1e-2 bound.  Host only. */
+int na_bf16_precise(const na_problem* p);
 
 /* Static description of a status code. */
 const char* na_status_string(na_status s);

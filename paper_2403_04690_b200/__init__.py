@@ -7,13 +7,14 @@ the ABI (pointers, sizes, the current CUDA stream) and does no arithmetic.
 If the library is missing the import fails loudly; there is no CPU fallback.
 """
 from .na import (NA_BF16, NA_F16, NA_F32, NA_IMPL_AUTO, NA_IMPL_SIMT, NA_IMPL_TC, NAError,
-                 Problem, last_launch_count, lib, make_problem, na_bwd, na_bwd_workspace_size,
+                 Problem, last_launch_count, lib, make_problem, na_bf16_precise, na_bwd,
+                 na_bwd_workspace_size,
                  na_fwd, na_get_plan_choice, na_plan_candidates, na_selected_impl,
                  na_set_plan_choice, na_tune, na_validate, profile_collect, profile_enable,
                  status_string)
 
 __all__ = ["NA_BF16", "NA_F16", "NA_F32", "NA_IMPL_AUTO", "NA_IMPL_SIMT", "NA_IMPL_TC", "NAError",
-           "Problem", "last_launch_count", "lib", "make_problem", "na_bwd",
+           "Problem", "last_launch_count", "lib", "make_problem", "na_bf16_precise", "na_bwd",
            "na_bwd_workspace_size", "na_fwd", "na_get_plan_choice", "na_plan_candidates",
            "na_selected_impl", "na_set_plan_choice", "na_tune", "na_validate", "profile_collect",
            "profile_enable", "status_string"]

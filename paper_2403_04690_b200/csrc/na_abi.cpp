@@ -211,6 +211,14 @@ int na_selected_impl(const na_problem* p) {
   return select_impl(p, g, &why);
 }
 
+int na_bf16_precise(const na_problem* p) {
+  if (validate(p) != NA_OK) return -1;
+  na::Geom g = make_geom(p);
+  const char* why;
+  if (p->dtype != NA_BF16 || select_impl(p, g, &why) != NA_IMPL_TC) return 0;
+  return na::bf16_precise(g) ? 1 : 0;
+}
+
 na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* v, void* o,
                  float* lse, void* stream) {
   na_status s = validate(p);

@@ -41,6 +41,21 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
 // tcgen05 path.  tc_supported() is a pure host check; the launchers return
 // cudaErrorNotSupported for problems outside it.
 bool tc_supported(int dtype, const Geom& g, const char** why);
+// bf16 only: whether the kernels take the error-compensated variant (DESIGN.md
+// R13): the forward normalises O by the sum of the bf16-rounded P, the
+// backward splits its bf16 P / dS MMA operands hi + lo and corrects D_x in
+// the dQ kernel.  It is needed where outputs can reach magnitudes >= 2,
+// whose bf16 half-ulp (2^-8 .. 2^-7) leaves < 0.0022 of the 1e-2 bound for
+// the 2^-9-relative rounding of P / dS: with few keys per window single
+// probabilities approach 1 and gradients concentrate.  Every window holds
+// at least prod over NON-causal axes of k keys (a causal axis leaves its
+// first query one key); below kBf16PlainMinKeys the precise variant runs.
+// Measured on unit-normal data (profiles/r02_bf16_variants.md): the plain
+// variant exceeds the bound at 35-75 keys (dK/dV up to 0.013) and stays
+// within it with >= 0.0033 to spare at 169-255 keys (config D: backward
+// 0.94 vs 1.64 ms).
+constexpr int kBf16PlainMinKeys = 128;
+bool bf16_precise(const Geom& g);
 // Opt a kernel into `bytes` of dynamic shared memory on the current device
 // (once per kernel and device; thread-safe).
 cudaError_t ensure_smem_attr(const void* func, int bytes);

@@ -114,7 +114,7 @@ struct BwdMaps {
   CUtensorMap o;  // dQ: the stationary tile's O rows (fused preprocess)
 };
 
-template <int RANK, int D, bool BF16, bool KV_STATIONARY>
+template <int RANK, int D, bool BF16, bool KV_STATIONARY, bool PRECISE>
 __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, const TcPlan& pl,
                                          float* __restrict__ rv, const float* __restrict__ lse,
                                          unsigned num_tiles) {
@@ -139,12 +139,13 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   // row vectors the dK/dV kernel (run next) reads.  Dt_x keeps the large
   // first term free of cancellation; c_x is small.  fp16's stored O is 8x
   // finer and keeps Dt_x.
-  constexpr bool kExactD = !KV_STATIONARY && BF16;
+  // Only in the PRECISE variant (bf16_precise(): some window is small).
+  constexpr bool kExactD = !KV_STATIONARY && BF16 && PRECISE;
   // bf16 (R13): the 16-bit A operands of the OUT MMAs (P, dS) are
   // split hi + lo, x = bf16(x) + bf16(x - bf16(x)), and both halves are
   // multiplied (a second MMA into the same accumulator), so the products
   // carry ~2^-17 instead of 2^-9 relative error; fp16's 2^-12 needs no split.
-  constexpr bool kSplit = BF16;
+  constexpr bool kSplit = BF16 && PRECISE;
   using S = BwdSmem<D, KV_STATIONARY, kFuse, kExactD>;
   constexpr int kStages = S::kSt;
   // Output accumulator columns per tile; double-buffered when two fit.
@@ -883,32 +884,32 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
 }
 
 // dK, dV: key-stationary over the inverse halo.
-template <int RANK, int D, bool BF16>
+template <int RANK, int D, bool BF16, bool PRECISE>
 __global__ void __launch_bounds__(kThreads, 1)
     fna_dkdv_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, float* __restrict__ rv,
                 unsigned num_tiles) {
-  bwd_body<RANK, D, BF16, true>(maps, g, pl, rv, nullptr, num_tiles);
+  bwd_body<RANK, D, BF16, true, PRECISE>(maps, g, pl, rv, nullptr, num_tiles);
 }
 
 // dQ: query-stationary over the forward halo.
-template <int RANK, int D, bool BF16>
+template <int RANK, int D, bool BF16, bool PRECISE>
 __global__ void __launch_bounds__(kThreads, 1)
     fna_dq_tc(const __grid_constant__ BwdMaps maps, Geom g, TcPlan pl, float* __restrict__ rv,
               const float* __restrict__ lse, unsigned num_tiles) {
-  bwd_body<RANK, D, BF16, false>(maps, g, pl, rv, lse, num_tiles);
+  bwd_body<RANK, D, BF16, false, PRECISE>(maps, g, pl, rv, lse, num_tiles);
 }
 
 // Everything that can fail on the host (function attributes; the tensor maps
 // are encoded by the caller) happens before the first launch, so an error
 // leaves the stream and the workspace untouched (include/na.h).
-template <int RANK, int D, bool BF16>
+template <int RANK, int D, bool BF16, bool PRECISE = false>
 cudaError_t launch_all(int dtype, const Geom& g, const TcPlan* pls, const BwdMaps& mkv, const BwdMaps& mq,
                        const void* o, const void* d_o, float* rv, const float* lse, cudaStream_t st) {
   constexpr bool kFuse = RANK == 1;  // dQ forms the row vectors (see bwd_body)
   const int smem_kv = BwdSmem<D, true, false>::kBytes + 1024;
-  const int smem_q = BwdSmem<D, false, kFuse, BF16>::kBytes + 1024;
-  auto kdkdv = fna_dkdv_tc<RANK, D, BF16>;
-  auto kdq = fna_dq_tc<RANK, D, BF16>;
+  const int smem_q = BwdSmem<D, false, kFuse, BF16 && PRECISE>::kBytes + 1024;
+  auto kdkdv = fna_dkdv_tc<RANK, D, BF16, PRECISE>;
+  auto kdq = fna_dq_tc<RANK, D, BF16, PRECISE>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kdkdv), smem_kv);
   if (e != cudaSuccess) return e;
   if ((e = ensure_smem_attr(reinterpret_cast<const void*>(kdq), smem_q)) != cudaSuccess) return e;
@@ -938,15 +939,20 @@ cudaError_t launch_all(int dtype, const Geom& g, const TcPlan* pls, const BwdMap
 template <int RANK>
 cudaError_t by_type(int dtype, const Geom& g, const TcPlan* pl, const BwdMaps& mkv, const BwdMaps& mq,
                     const void* o, const void* d_o, float* rv, const float* lse, cudaStream_t st) {
-  const bool bf = dtype == 2;
-  if (g.D == 64)
-    return bf ? launch_all<RANK, 64, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
-              : launch_all<RANK, 64, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
-  if (g.D == 16)
-    return bf ? launch_all<RANK, 16, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
-              : launch_all<RANK, 16, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
-  return bf ? launch_all<RANK, 32, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
-            : launch_all<RANK, 32, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+  if (dtype == 2) {
+    const bool pr = bf16_precise(g);
+    if (g.D == 64)
+      return pr ? launch_all<RANK, 64, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
+                : launch_all<RANK, 64, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+    if (g.D == 16)
+      return pr ? launch_all<RANK, 16, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
+                : launch_all<RANK, 16, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+    return pr ? launch_all<RANK, 32, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
+              : launch_all<RANK, 32, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+  }
+  if (g.D == 64) return launch_all<RANK, 64, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+  if (g.D == 16) return launch_all<RANK, 16, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+  return launch_all<RANK, 32, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
 }
 
 }  // namespace

@@ -42,6 +42,17 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
   }
 }
 
+// acc + the two bf16 halves of w, each in fp32 (one mixed-precision
+// add.f32.bf16 per half, FHADD.BF16 with a half selector in SASS; no unpack).
+__device__ __forceinline__ float2 add_bf16x2(float2 acc, uint32_t w) {
+  float2 r;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+      "add.rn.f32.bf16 %0, l, %3;\n\tadd.rn.f32.bf16 %1, h, %4;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(w), "f"(acc.x), "f"(acc.y));
+  return r;
+}
+
 // 2^x for a pair of values on the FMA pipe (the MUFU ex2 unit is the
 // scarcest resource of the softmax): Cody-Waite split x = n + f with
 // n = rint(x), f in [-0.5, 0.5]; 2^f by a degree-3 polynomial with c0 = 1

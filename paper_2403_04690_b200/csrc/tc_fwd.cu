@@ -98,7 +98,9 @@ struct FwdMaps {
   CUtensorMap q, k, v, o;
 };
 
-template <int RANK, int D, bool BF16>
+// PRECISE (bf16 only, bf16_precise()): O normalised by the sum of the
+// bf16-rounded P (R13).
+template <int RANK, int D, bool BF16, bool PRECISE>
 __global__ void __launch_bounds__(kThreads, 2)
     fna_fwd_tc(const __grid_constant__ FwdMaps maps, Geom g, TcPlan pl, float* __restrict__ lse,
                unsigned num_tiles) {
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const CUtensorMap& map_v = maps.v;
   const CUtensorMap& map_o = maps.o;
   using S = FwdSmem<D>;
-  using T = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
+  constexpr bool kSumRounded = BF16 && PRECISE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared address space (LDS/STS, not generic LD/ST).
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             NA_TMEM_ST16(trow + kColO + c0, ov);
           }
           l *= f;
-          if constexpr (BF16) lr *= f;
+          if constexpr (kSumRounded) lr *= f;
         } else if (need) {
           l = 0.f;  // no valid key seen yet on this row
           lr = 0.f;
@@ -380,14 +382,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             acc1 = __fadd2_rn(acc1, p1);
             sv[16 * gq + (c >> 1)] = pack2<BF16>(p0.x, p0.y);
             sv[16 * gq + (c >> 1) + 1] = pack2<BF16>(p1.x, p1.y);
-            if constexpr (BF16) {
-              accr0 = __fadd2_rn(accr0, unpack2<BF16>(sv[16 * gq + (c >> 1)]));
-              accr1 = __fadd2_rn(accr1, unpack2<BF16>(sv[16 * gq + (c >> 1) + 1]));
+            if constexpr (kSumRounded) {
+              accr0 = add_bf16x2(accr0, sv[16 * gq + (c >> 1)]);
+              accr1 = add_bf16x2(accr1, sv[16 * gq + (c >> 1) + 1]);
             }
           }
         }
         l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
-        if constexpr (BF16) lr += (accr0.x + accr0.y) + (accr1.x + accr1.y);
+        if constexpr (kSumRounded) lr += (accr0.x + accr0.y) + (accr1.x + accr1.y);
         if (tracer) NA_TRACE_EV(2, tr, 26);
         // P into its buffer once PV_{kv-1} has read the previous P
         if (kv > 0) ptx::mbar_wait(bar + B_PF, (kv - 1) & 1);
@@ -411,10 +413,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       ptx::mbar_wait(bar + B_OF, ti & 1);
       ptx::tc_fence_after();
       if (tracer) NA_TRACE_EV(2, tr, 22);
-      // bf16: O = sum bf16(P) v / sum bf16(P), a convex combination of the
-      // v's, so the 2^-9 rounding of P does not scale O (exact when one key
-      // dominates); fp16 P is 8x finer and uses l.
-      const float lo = BF16 ? lr : l;
+      // bf16 (PRECISE): O = sum bf16(P) v / sum bf16(P), a convex
+      // combination of the v's, so the 2^-9 rounding of P does not scale O
+      // (exact when one key dominates); fp16 P is 8x finer and uses l.
+      const float lo = kSumRounded ? lr : l;
       const float inv = lo > 0.f ? 1.f / lo : 0.f;
       const int qb = ti & 1;
       uint8_t* stage = smem + S::kQ + qb * S::kTile;
@@ -462,9 +464,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
-template <int RANK, int D, bool BF16>
+template <int RANK, int D, bool BF16, bool PRECISE = false>
 cudaError_t launch(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse, cudaStream_t st) {
-  auto kern = fna_fwd_tc<RANK, D, BF16>;
+  auto kern = fna_fwd_tc<RANK, D, BF16, PRECISE>;
   const int smem = FwdSmem<D>::kBytes + 1024;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
@@ -481,12 +483,17 @@ cudaError_t launch(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* 
 template <int RANK>
 cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse,
                     cudaStream_t st) {
-  const bool bf = dtype == 2;
-  if (g.D == 64) return bf ? launch<RANK, 64, true>(g, pl, maps, lse, st)
-                           : launch<RANK, 64, false>(g, pl, maps, lse, st);
-  if (g.D == 16) return bf ? launch<RANK, 16, true>(g, pl, maps, lse, st)
-                           : launch<RANK, 16, false>(g, pl, maps, lse, st);
-  return bf ? launch<RANK, 32, true>(g, pl, maps, lse, st) : launch<RANK, 32, false>(g, pl, maps, lse, st);
+  if (dtype == 2) {
+    const bool pr = bf16_precise(g);
+    if (g.D == 64) return pr ? launch<RANK, 64, true, true>(g, pl, maps, lse, st)
+                             : launch<RANK, 64, true>(g, pl, maps, lse, st);
+    if (g.D == 16) return pr ? launch<RANK, 16, true, true>(g, pl, maps, lse, st)
+                             : launch<RANK, 16, true>(g, pl, maps, lse, st);
+    return pr ? launch<RANK, 32, true, true>(g, pl, maps, lse, st) : launch<RANK, 32, true>(g, pl, maps, lse, st);
+  }
+  if (g.D == 64) return launch<RANK, 64, false>(g, pl, maps, lse, st);
+  if (g.D == 16) return launch<RANK, 16, false>(g, pl, maps, lse, st);
+  return launch<RANK, 32, false>(g, pl, maps, lse, st);
 }
 
 }  // namespace

@@ -33,6 +33,13 @@ bool tc_supported(int dtype, const Geom& g, const char** why) {
   return true;
 }
 
+bool bf16_precise(const Geom& g) {
+  long long keys = 1;  // keys every window holds at least
+  for (int a = 0; a < g.rank; ++a)
+    if (!g.causal[a]) keys *= g.k[a];
+  return keys < kBf16PlainMinKeys;
+}
+
 namespace {
 
 int ceil_div(int a, int b) { return (a + b - 1) / b; }

@@ -47,6 +47,7 @@ class NAError(RuntimeError):
 _lib = None
 
 EXPORTS = ("na_validate", "na_fwd", "na_bwd", "na_bwd_workspace_size", "na_selected_impl",
+           "na_bf16_precise",
            "na_status_string", "na_last_error", "na_last_launch_count", "na_profile_enable",
            "na_profile_collect", "na_kernel_name", "na_plan_candidates", "na_tune",
            "na_get_plan_choice", "na_set_plan_choice")
@@ -72,6 +73,8 @@ def lib():
         L.na_bwd_workspace_size.restype = ctypes.c_size_t
         L.na_selected_impl.argtypes = [P]
         L.na_selected_impl.restype = ctypes.c_int
+        L.na_bf16_precise.argtypes = [P]
+        L.na_bf16_precise.restype = ctypes.c_int
         L.na_status_string.argtypes = [ctypes.c_int]
         L.na_status_string.restype = ctypes.c_char_p
         L.na_last_error.argtypes = []
@@ -163,6 +166,11 @@ def na_validate(p: Problem) -> int:
 
 def na_selected_impl(p: Problem) -> int:
     return lib().na_selected_impl(ctypes.byref(p))
+
+
+def na_bf16_precise(p: Problem) -> int:
+    """1: the error-compensated bf16 kernel variant runs for p (R13)."""
+    return lib().na_bf16_precise(ctypes.byref(p))
 
 
 def na_bwd_workspace_size(p: Problem) -> int:

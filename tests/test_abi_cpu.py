@@ -107,6 +107,23 @@ def test_fp32_selects_simt(na):
     assert na.na_selected_impl(P(na, kernel_size=[4])) == -1
 
 
+def test_bf16_variant_rule(na):
+    """DESIGN.md R13: the error-compensated bf16 variant runs iff some window
+    holds < 128 keys (product of k over the non-causal axes)."""
+    bf = torch.bfloat16
+    assert na.na_bf16_precise(P(na, dtype=bf, extent=[300], kernel_size=[127])) == 1
+    assert na.na_bf16_precise(P(na, dtype=bf, extent=[300], kernel_size=[129])) == 0
+    assert na.na_bf16_precise(P(na, dtype=bf, extent=[300], kernel_size=[255], is_causal=[1])) == 1
+    assert na.na_bf16_precise(P(na, dtype=bf, extent=[128, 128], kernel_size=[13, 13],
+                                dilation=[2, 2])) == 0                      # config D
+    assert na.na_bf16_precise(P(na, dtype=bf, extent=[40, 40], kernel_size=[11, 11])) == 1
+    assert na.na_bf16_precise(P(na, dtype=bf, extent=[16, 40, 40], kernel_size=[7, 7, 7],
+                                is_causal=[1, 0, 0])) == 1                  # 49 keys at t = 0
+    assert na.na_bf16_precise(P(na, dtype=bf, extent=[16, 40, 40], kernel_size=[3, 7, 7])) == 0
+    assert na.na_bf16_precise(P(na, extent=[300], kernel_size=[7])) == 0     # fp16
+    assert na.na_bf16_precise(P(na, dtype=bf, kernel_size=[4])) == -1       # invalid
+
+
 def test_no_silent_fallback_for_16bit(na):
     """A 16-bit problem the tensor-core path cannot run is refused under AUTO
     (NA_ERR_IMPL before any launch) and runs on the CUDA cores only when asked."""
