@@ -61,10 +61,29 @@ constexpr int kMmaWarp = 7;
 // 2-CTA/SM budget of 256 threads x 128.
 constexpr uint32_t kRegsSoftmax = 200;
 constexpr uint32_t kRegsOther = 56;
+// Small-tile variant (SMALL: head_dim <= 32 and KV chunks of <= 64 keys,
+// e.g. 2-D 56x56 k=7 with dilation 8, one 7x7 class per tile): a tile is
+// one or two short rounds, so per-tile latency dominates and more tiles
+// must be in flight per SM.  S 64 + P 32 + O 32 TMEM columns -> 128 per
+// CTA, 3 CTAs per SM; registers 3 x 256 x 80 = 61440 split 120 / 40.
+// (4 CTAs per SM would leave 96 / 32 registers: ~650 bytes of spills.)
+constexpr uint32_t kRegsSoftmaxSmall = 120;
+constexpr uint32_t kRegsOtherSmall = 40;
 // TMEM columns (256 per CTA, two CTAs per SM): S [0, 128) fp32 logits of the
 // current round; P [128, 192) the previous round's probabilities as packed
 // 16-bit pairs (A operand of PV); O [192, 192 + D) the fp32 accumulator.
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
+constexpr uint32_t kColPSmall = 64, kColOSmall = 96;
+template <bool SMALL>
+struct FwdCfg {
+  static constexpr int kCtas = SMALL ? 3 : 2;            // CTAs per SM
+  static constexpr uint32_t kTmemCols = SMALL ? 128 : 256;
+  static constexpr uint32_t kColP_ = SMALL ? kColPSmall : kColP;
+  static constexpr uint32_t kColO_ = SMALL ? kColOSmall : kColO;
+  static constexpr int kGroups = SMALL ? 2 : 4;          // 32-column groups of a round
+  static constexpr uint32_t kRegsS = SMALL ? kRegsSoftmaxSmall : kRegsSoftmax;
+  static constexpr uint32_t kRegsO = SMALL ? kRegsOtherSmall : kRegsOther;
+};
 
 template <int D>
 struct FwdSmem {
@@ -100,8 +119,8 @@ struct FwdMaps {
 
 // PRECISE (bf16 only, bf16_precise()): O normalised by the sum of the
 // bf16-rounded P (R13).
-template <int RANK, int D, bool BF16, bool PRECISE>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int RANK, int D, bool BF16, bool PRECISE, bool SMALL>
+__global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
     fna_fwd_tc(const __grid_constant__ FwdMaps maps, Geom g, TcPlan pl, float* __restrict__ lse,
                unsigned num_tiles) {
   const CUtensorMap& map_q = maps.q;
@@ -110,6 +129,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   const CUtensorMap& map_o = maps.o;
   using S = FwdSmem<D>;
   constexpr bool kSumRounded = BF16 && PRECISE;
+  using C = FwdCfg<SMALL>;
+  constexpr uint32_t kColP = C::kColP_, kColO = C::kColO_;
+  constexpr int kG = C::kGroups;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared address space (LDS/STS, not generic LD/ST).
@@ -147,14 +169,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     ptx::fence_proxy_async();
   }
-  if (warp == kMmaWarp) ptx::tmem_alloc<256>(tmem_slot);
+  if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp >= 4) {
-  ptx::setmaxnreg_dec<kRegsOther>();
+  ptx::setmaxnreg_dec<C::kRegsO>();
   if (warp == kProducerWarp) {
     // ===================== TMA producer (whole warp, one lane issues) =====================
     ptx::tma_prefetch(&map_q);
@@ -262,13 +284,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   }
   } else {
-    ptx::setmaxnreg_inc<kRegsSoftmax>();
+    ptx::setmaxnreg_inc<C::kRegsS>();
     // ===================== softmax / epilogue (128 threads) =====================
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float sl2 = g.scale_log2;
-    const bool wide = pl.n_kv > 64;  // P needs TMEM columns [32, 64) too
+    const bool wide = !SMALL && pl.n_kv > 64;  // P needs TMEM columns [32, 64) too
     uint32_t kv = 0, ti = 0;
     int tr = 0;
     const bool tracer = warp == 2;
@@ -286,9 +308,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       r.chunk_mask(pl, org, mw);
       for (int j = 0; j < t.nchunks; ++j, ++kv) {
         // warp-uniform group flags before the wait (they depend on the mask only)
-        bool live[4], full[4];
+        bool live[kG], full[kG];
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) {
+        for (int gq = 0; gq < kG; ++gq) {
           live[gq] = __any_sync(0xffffffffu, mw[gq] != 0u);
           full[gq] = __all_sync(0xffffffffu, mw[gq] == 0xffffffffu);
         }
@@ -297,9 +319,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (tracer) NA_TRACE_EV(2, tr, 20);
         // The whole round (<= 128 logits of this row) in registers: one
         // tcgen05.wait for all loads, independent chains across the groups.
-        uint32_t sv[128];
+        uint32_t sv[32 * kG];
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq)
+        for (int gq = 0; gq < kG; ++gq)
           if (live[gq]) NA_TMEM_LD32(trow + kColS + 32 * gq, (sv + 32 * gq));
         // the next chunk's mask, in the shadow of the TMEM load latency
         uint32_t mwn[4] = {0u, 0u, 0u, 0u};
@@ -314,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // mask (only partially valid groups) and row max of the raw logits
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) {
+        for (int gq = 0; gq < kG; ++gq) {
           if (!live[gq]) continue;
           const uint32_t w = mw[gq];
           if (!full[gq]) {
@@ -362,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // exponentials; P packed as 16-bit pairs IN PLACE: the pair of
         // columns (2i, 2i+1) goes to sv[i], whose logit was already consumed
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) {
+        for (int gq = 0; gq < kG; ++gq) {
           if (!live[gq]) {
 #pragma unroll
             for (int c = 0; c < 16; ++c) sv[16 * gq + c] = 0u;
@@ -460,24 +482,33 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<256>(tmem);
+    ptx::tmem_dealloc<C::kTmemCols>(tmem);
   }
 }
 
-template <int RANK, int D, bool BF16, bool PRECISE = false>
-cudaError_t launch(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse, cudaStream_t st) {
-  auto kern = fna_fwd_tc<RANK, D, BF16, PRECISE>;
+template <int RANK, int D, bool BF16, bool PRECISE, bool SMALL>
+cudaError_t launch_v(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse, cudaStream_t st) {
+  auto kern = fna_fwd_tc<RANK, D, BF16, PRECISE, SMALL>;
   const int smem = FwdSmem<D>::kBytes + 1024;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const long long tiles = (long long)g.BH * pl.nres * pl.tiles;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  const long long per = 2;  // CTAs per SM (TMEM: 256 columns each)
+  const long long per = FwdCfg<SMALL>::kCtas;  // CTAs per SM (TMEM columns each: kTmemCols)
   const unsigned grid = (unsigned)(tiles < per * num_sms() ? tiles : per * num_sms());
   prof_begin(KID_FWD_TC, st);
   kern<<<grid, kThreads, smem, st>>>(maps, g, pl, lse, (unsigned)tiles);
   prof_end(st);
   return cudaGetLastError();
+}
+
+// The small-tile variant needs S 64 + P 32 + O <= 32 TMEM columns.
+template <int RANK, int D, bool BF16, bool PRECISE = false>
+cudaError_t launch(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse, cudaStream_t st) {
+  if constexpr (D <= 32) {
+    if (pl.n_kv <= 64) return launch_v<RANK, D, BF16, PRECISE, true>(g, pl, maps, lse, st);
+  }
+  return launch_v<RANK, D, BF16, PRECISE, false>(g, pl, maps, lse, st);
 }
 
 template <int RANK>

@@ -81,14 +81,18 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand)
     // (0 = the model's choice; na_tune measures the others).  The per-round
     // cost (in MMA columns) was calibrated on the BASELINE configs.
     constexpr int kRoundCols = 96;
-    const int pick = std::min(std::max(pick_in, 0), kTopPlans - 1);
+    const int pick = std::min(std::max(pick_in, 0), kMaxPlans - 1);
     const int R = g.rank;
     struct Cand {
       double cost;
       int tq[3], ck[3];
     };
-    Cand top[kTopPlans];
+    Cand top[kMaxPlans];
     int ntop = 0;
+    // head_dim <= 32: the cheapest plan with KV chunks of <= 64 keys is also
+    // a candidate (the forward runs those with 3 CTAs per SM, tc_fwd.cu),
+    // whatever the model says; na_tune measures it against the others.
+    Cand small{1e300, {1, 1, 1}, {1, 1, 1}};
     auto consider = [&](const int tq[3]) {
       int h[3] = {1, 1, 1}, valid_rows = 1;
       for (int a = 0; a < R; ++a) {
@@ -116,6 +120,13 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand)
             int chunks = 1;
             for (int a = 0; a < R; ++a) chunks *= ceil_div(h[a], ck[a]);
             const double cost = (double)chunks * (round16(rows) + kRoundCols) / valid_rows;
+            if (rows <= 64 && cost < small.cost) {
+              small.cost = cost;
+              for (int a = 0; a < 3; ++a) {
+                small.tq[a] = a < R ? tq[a] : 1;
+                small.ck[a] = a < R ? ck[a] : 1;
+              }
+            }
             // keep the kTopPlans cheapest candidates, sorted
             if (ntop < kTopPlans || cost < top[ntop - 1].cost) {
               int i = ntop < kTopPlans ? ntop++ : kTopPlans - 1;
@@ -146,6 +157,11 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand)
           t[0] = tile_rows / (tx * ty);
           consider(t);
         }
+    }
+    if (g.D <= 32 && small.cost < 1e300) {
+      bool have = false;
+      for (int i = 0; i < ntop; ++i) have = have || top[i].ck[0] * top[i].ck[1] * top[i].ck[2] <= 64;
+      if (!have) top[ntop++] = small;  // an extra candidate (kMaxPlans = kTopPlans + 1)
     }
     if (ncand) *ncand = ntop;
     const Cand& c = top[std::min(pick, ntop - 1)];
@@ -210,7 +226,7 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand)
 // (small linear table, mutex).
 namespace {
 struct PlanEntry {
-  int key[15];
+  int key[16];
   TcPlan plan;
   int ncand;
 };
@@ -230,13 +246,14 @@ void geom_key(const Geom& g, int tile_rows, int* key) {
 }  // namespace
 
 TcPlan make_plan(const Geom& g, int tile_rows, int pick, int* ncand) {
-  int key[15];
+  int key[16];
   geom_key(g, tile_rows, key);
   key[14] = pick;
+  key[15] = g.D <= 32;  // the candidate list depends on it (small-chunk plan)
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (const PlanEntry& e : g_plans)
-      if (std::equal(key, key + 15, e.key)) {
+      if (std::equal(key, key + 16, e.key)) {
         if (ncand) *ncand = e.ncand;
         return e.plan;
       }
@@ -247,7 +264,7 @@ TcPlan make_plan(const Geom& g, int tile_rows, int pick, int* ncand) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
   if (g_plans.size() >= 512) g_plans.erase(g_plans.begin());
   PlanEntry e;
-  std::copy(key, key + 15, e.key);
+  std::copy(key, key + 16, e.key);
   e.plan = pl;
   e.ncand = nc;
   g_plans.push_back(e);

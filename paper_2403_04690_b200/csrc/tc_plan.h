@@ -34,6 +34,7 @@ __device__ __forceinline__ uint32_t fmod_(uint32_t n, uint32_t q, const FastDiv&
 #endif
 
 constexpr int kTopPlans = 4;  // planner candidates kept for measurement (na_tune)
+constexpr int kMaxPlans = kTopPlans + 1;  // + the best small-chunk plan (head_dim <= 32)
 
 // Which candidate plan each tensor-core kernel uses.
 struct PlanChoice {
