@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restri
                                                        const T* __restrict__ d_o,
                                                        float* __restrict__ Dvec,
                                                        const float* __restrict__ lse, RvDiv f) {
-  // D/8 threads per row; only the tensor-core path (D in {32, 64}) launches
-  // this kernel, so tpr is a power of two: shift/mask, no 64-bit division.
+  // D/8 threads per row; only the tensor-core path (D in {16, 32, 64, 128})
+  // launches this kernel, so tpr is a power of two: shift/mask, no 64-bit division.
   // Each thread covers kPreRows rows (one per 256/tpr-row slab of the block),
   // all loads issued before any arithmetic: more bytes in flight per thread
   // (2 for rank 1; the multi-dimensional slot arithmetic prefers 1).

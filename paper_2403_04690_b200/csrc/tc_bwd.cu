@@ -67,16 +67,26 @@ constexpr float kLog2e = 1.4426950408889634f;
 // Both kernels stream 4 stages; a fused dQ (FUSE: rank 1) holds the O tiles
 // it reads to form the row vectors itself (see the dQ compute warps) where
 // dK/dV keeps the gathered row vectors of its streamed chunks.
+// head_dim 128 ("wide"): every tile is stored as two 64-column SW128 halves
+// [half][rows][128 B] (as in the forward); streamed chunks hold <= 64
+// partner rows (planner), two stages, so the stationary double buffer
+// (128 KB) and the ring (64 KB) fit.
 template <int D, bool KV, bool FUSE, bool EXACT = false>
 struct BwdSmem {
-  static constexpr int kSt = 4;                       // streamed stages
-  static constexpr int kRowBytes = D * 2;
-  static constexpr int kTile = 128 * kRowBytes;
+  static constexpr bool kWide = D > 64;
+  static constexpr int kHalves = kWide ? 2 : 1;
+  static constexpr int kSt = kWide ? 2 : 4;           // streamed stages
+  static constexpr int kRowBytes = (kWide ? 64 : D) * 2;  // one swizzled row (of one half)
+  static constexpr int kBRows = kWide ? 64 : 128;     // streamed rows per tile
+  static constexpr int kAHalf = 128 * kRowBytes;
+  static constexpr int kTile = kHalves * kAHalf;      // stationary tile
+  static constexpr int kBHalf = kBRows * kRowBytes;
+  static constexpr int kBTile = kHalves * kBHalf;     // streamed tile
   static constexpr int kA = 0;                        // stationary [2 bufs][2 tiles] (K,V | Q,dO)
   static constexpr int kO = kA + 4 * kTile;           // fused dQ: stationary O tile [2 bufs]
   static constexpr int kB0 = kO + (FUSE ? 2 * kTile : 0);  // streamed [kSt] (Q | K)
-  static constexpr int kB1 = kB0 + kSt * kTile;       // streamed [kSt] (dO | V)
-  static constexpr int kVec = kB1 + kSt * kTile;      // [kSt][-LSE2 x128 | D x128] fp32 (dK/dV)
+  static constexpr int kB1 = kB0 + kSt * kBTile;      // streamed [kSt] (dO | V)
+  static constexpr int kVec = kB1 + kSt * kBTile;     // [kSt][-LSE2 x128 | D x128] fp32 (dK/dV)
   static constexpr int kBar = kVec + (KV ? kSt * 256 * 4 : 0);
   static constexpr int kDx = kBar + 256;              // exact-D dQ: [2 groups][128] fp32 partials
   static constexpr int kBytes = kDx + (EXACT ? 2 * 128 * 4 : 0);
@@ -91,6 +101,13 @@ struct BwdSmem {
 // dK | dV (2D columns, single-buffered when 2D = 128) or dQ (D columns,
 // double-buffered).
 constexpr uint32_t kColOut = 384;
+// head_dim 128: two sub-chunk buffers [0, 256), outputs [256, 512) (dK | dV
+// = 2 x 128 columns; dQ 128 + the exact-D PK accumulator 128).
+template <int D>
+struct BwdTmem {
+  static constexpr uint32_t kNB = D > 64 ? 2 : 3;  // rotating S/dP sub-chunk buffers
+  static constexpr uint32_t kOut = kNB * 128;
+};
 
 enum : int {
   B_AF = 0,                 // stationary tiles full [2]
@@ -127,7 +144,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   // dQ forms the row vectors itself (fused preprocess) for rank 1; for
   // multi-dimensional tiles the extra per-tile work measured slower than the
   // separate preprocess pass, so there dQ reads them.
-  constexpr bool kFuse = !KV_STATIONARY && RANK == 1;
+  constexpr bool kFuse = !KV_STATIONARY && RANK == 1 && D <= 64;
   // bf16 dQ (R12): D_x is corrected in-kernel to sum_y P_xy dP_xy.
   // The row value read at the tile start, Dt_x = <dO_x, O_x> from the
   // stored (bf16-rounded) O, is only an estimate; the compute warps also
@@ -147,6 +164,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   // carry ~2^-17 instead of 2^-9 relative error; fp16's 2^-12 needs no split.
   constexpr bool kSplit = BF16 && PRECISE;
   using S = BwdSmem<D, KV_STATIONARY, kFuse, kExactD>;
+  constexpr uint32_t kNB = BwdTmem<D>::kNB, kColOut = BwdTmem<D>::kOut;
   constexpr int kStages = S::kSt;
   // Output accumulator columns per tile; double-buffered when two fit.
   constexpr int kOutCols = (KV_STATIONARY || kExactD) ? 2 * D : D;
@@ -187,11 +205,11 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     for (int i = threadIdx.x; i < kStages * 256; i += kThreads) vec[i] = 0.f;  // unloaded columns read 0
   }
   ptx::fence_proxy_async();  // before TMA writes the same smem
-  if (pl.rows_kv < 128) {  // rows no TMA box writes must be finite (zero)
-    const int nz = (128 - pl.rows_kv) * S::kRowBytes / 16;
-    for (int i = threadIdx.x; i < 2 * kStages * nz; i += kThreads) {
-      const int buf = i / nz, off = i % nz;
-      uint4* base = reinterpret_cast<uint4*>(smem + S::kB0 + buf * S::kTile + pl.rows_kv * S::kRowBytes);
+  if (pl.rows_kv < S::kBRows) {  // rows no TMA box writes must be finite (zero)
+    const int nz = (S::kBRows - pl.rows_kv) * S::kRowBytes / 16;
+    for (int i = threadIdx.x; i < 2 * kStages * S::kHalves * nz; i += kThreads) {
+      const int buf = i / nz, off = i % nz;  // (tensor, stage) x half
+      uint4* base = reinterpret_cast<uint4*>(smem + S::kB0 + buf * S::kBHalf + pl.rows_kv * S::kRowBytes);
       base[off] = make_uint4(0, 0, 0, 0);
     }
     ptx::fence_proxy_async();
@@ -208,7 +226,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     ptx::tma_prefetch(&map_a1);
     ptx::tma_prefetch(&map_b0);
     ptx::tma_prefetch(&map_b1);
-    const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes;
+    const uint32_t bytes = 2 * pl.rows_kv * S::kRowBytes * S::kHalves;
     // dK/dV: the streamed chunk's row vectors (-LSE*log2(e), D) are gathered
     // with 4-byte cp.async by the 32 producer lanes (columns lane, lane+32,
     // ...): chunk origins need no 16-byte alignment, unlike a TMA box.
@@ -224,12 +242,15 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       if (NA_BWD_TRACE_ON) NA_TRACE_EV(0, tr, 1);
       uint8_t* a0 = smem + S::kA + (2 * ab) * S::kTile;
       uint8_t* a1 = a0 + S::kTile;
-      ptx::mbar_expect_tx_w(bar + B_AF + ab, (kFuse ? 3 : 2) * 128 * S::kRowBytes);
+      ptx::mbar_expect_tx_w(bar + B_AF + ab, (kFuse ? 3 : 2) * S::kTile);
+      for (int h = 0; h < S::kHalves; ++h)
+        for (int i = 0; i < pl.q_issues; ++i) {
+          t.template load_box<RANK>(&map_a0, a0 + h * S::kAHalf + i * pl.q_box_x * S::kRowBytes, bar + B_AF + ab,
+                                    t.q_origin, i * pl.q_box_x, g, 64 * h);
+          t.template load_box<RANK>(&map_a1, a1 + h * S::kAHalf + i * pl.q_box_x * S::kRowBytes, bar + B_AF + ab,
+                                    t.q_origin, i * pl.q_box_x, g, 64 * h);
+        }
       for (int i = 0; i < pl.q_issues; ++i) {
-        t.template load_box<RANK>(&map_a0, a0 + i * pl.q_box_x * S::kRowBytes, bar + B_AF + ab,
-                                  t.q_origin, i * pl.q_box_x, g);
-        t.template load_box<RANK>(&map_a1, a1 + i * pl.q_box_x * S::kRowBytes, bar + B_AF + ab,
-                                  t.q_origin, i * pl.q_box_x, g);
         if constexpr (kFuse)
           t.template load_box<RANK>(&maps.o, smem + S::kO + ab * S::kTile + i * pl.q_box_x * S::kRowBytes,
                                     bar + B_AF + ab, t.q_origin, i * pl.q_box_x, g);
@@ -241,12 +262,15 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         int org[3];
         t.chunk_origin(pl, j, org);
         ptx::mbar_expect_tx_w(bar + B_B + s, bytes);
-        for (int i = 0; i < pl.kv_issues; ++i) {
-          t.template load_box<RANK>(&map_b0, smem + S::kB0 + s * S::kTile + i * pl.kv_box_x * S::kRowBytes,
-                                    bar + B_B + s, org, i * pl.kv_box_x, g);
-          t.template load_box<RANK>(&map_b1, smem + S::kB1 + s * S::kTile + i * pl.kv_box_x * S::kRowBytes,
-                                    bar + B_B + s, org, i * pl.kv_box_x, g);
-        }
+        for (int h = 0; h < S::kHalves; ++h)
+          for (int i = 0; i < pl.kv_issues; ++i) {
+            t.template load_box<RANK>(&map_b0,
+                                      smem + S::kB0 + s * S::kBTile + h * S::kBHalf + i * pl.kv_box_x * S::kRowBytes,
+                                      bar + B_B + s, org, i * pl.kv_box_x, g, 64 * h);
+            t.template load_box<RANK>(&map_b1,
+                                      smem + S::kB1 + s * S::kBTile + h * S::kBHalf + i * pl.kv_box_x * S::kRowBytes,
+                                      bar + B_B + s, org, i * pl.kv_box_x, g, 64 * h);
+          }
         if constexpr (KV_STATIONARY) {
           const float* src = rv + rv_base(g, t.bh, t.res);
           float* dst = vec + s * 256;
@@ -313,23 +337,25 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         for (int c_u = 0; c_u < nsub; ++c_u) {
           const uint32_t kv = c_kv + c_u / ns, gu = c_ub + c_u;
           const int h = c_u % ns, s = kv % kStages;
-          const uint32_t b3 = gu % 3, r3 = gu / 3;
-          if (gu >= 3) ptx::mbar_wait(bar + B_PE + b3, (r3 - 1) & 1);  // buffer's previous OUT done
+          const uint32_t b3 = gu % kNB, r3 = gu / kNB;
+          if (gu >= kNB) ptx::mbar_wait(bar + B_PE + b3, (r3 - 1) & 1);  // buffer's previous OUT done
           if (c_u == 0) ptx::mbar_wait(bar + B_AF + ab, (c_ti >> 1) & 1);
           if (h == 0) ptx::mbar_wait(bar + B_B + s, (kv / kStages) & 1);
           ptx::tc_fence_after();
           const uint32_t off = h * 64 * S::kRowBytes;
-          const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
-          const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
+          const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kBTile) + off;
+          const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kBTile) + off;
           const uint32_t id = h ? idesc_s1 : idesc_s0;
           const uint32_t buf = b3 * 128;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             // KV-stationary: S^T = K Q^T, dP^T = V dO^T.  Q-stationary: S = Q K^T, dP = dO V^T.
-            ptx::mma_ss_w(tmem + buf, ptx::make_sdesc(a0 + kk * 32, 16, kSbo, kSw),
-                          ptx::make_sdesc(b0 + kk * 32, 16, kSbo, kSw), id, kk > 0);
-            ptx::mma_ss_w(tmem + buf + 64, ptx::make_sdesc(a1 + kk * 32, 16, kSbo, kSw),
-                          ptx::make_sdesc(b1 + kk * 32, 16, kSbo, kSw), id, kk > 0);
+            // (head_dim 128: K-steps 4..7 read the second 64-column halves)
+            const uint32_t ha = (kk >> 2) * S::kAHalf, hb = (kk >> 2) * S::kBHalf, ko = (kk & 3) * 32;
+            ptx::mma_ss_w(tmem + buf, ptx::make_sdesc(a0 + ha + ko, 16, kSbo, kSw),
+                          ptx::make_sdesc(b0 + hb + ko, 16, kSbo, kSw), id, kk > 0);
+            ptx::mma_ss_w(tmem + buf + 64, ptx::make_sdesc(a1 + ha + ko, 16, kSbo, kSw),
+                          ptx::make_sdesc(b1 + hb + ko, 16, kSbo, kSw), id, kk > 0);
           }
           ptx::mma_commit_w(bar + B_S + b3);
         }
@@ -352,11 +378,11 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           const int h = u % ns, s = kv % kStages;
           const int width = h ? n1 : (ns == 2 ? 64 : pl.n_kv);
           const uint32_t off = h * 64 * S::kRowBytes;
-          const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kTile) + off;
-          const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kTile) + off;
-          const uint32_t b3 = gu % 3;
+          const uint32_t b0 = ptx::smem_u32(smem + S::kB0 + s * S::kBTile) + off;
+          const uint32_t b1 = ptx::smem_u32(smem + S::kB1 + s * S::kBTile) + off;
+          const uint32_t b3 = gu % kNB;
           const uint32_t pk = tmem + b3 * 128;  // P^T over S, dS^T over dP (in place)
-          ptx::mbar_wait(bar + B_P + b3, (gu / 3) & 1);
+          ptx::mbar_wait(bar + B_P + b3, (gu / kNB) & 1);
           if (NA_BWD_TRACE_ON) NA_TRACE_EV(1, tr, 11);
           if (u == 0) {  // the tile's first OUT MMA overwrites the output buffer: drained?
             if (kOutDouble) {
@@ -375,15 +401,16 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
             const uint32_t ca = kSplit ? 32 * (kk >> 1) + 8 * (kk & 1) : 8 * kk;
             if constexpr (KV_STATIONARY) {
               // dV += P^T dO ; dK += dS^T Q   (B operands MN-major; bf16: hi + lo)
-              const uint64_t dod = ptx::make_sdesc(b1 + boff, 128 * S::kRowBytes, kSbo, kSw);
-              const uint64_t qd = ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw);
+              // (LBO: the second 64-column atom of a head_dim 128 row, one half on)
+              const uint64_t dod = ptx::make_sdesc(b1 + boff, S::kBHalf, kSbo, kSw);
+              const uint64_t qd = ptx::make_sdesc(b0 + boff, S::kBHalf, kSbo, kSw);
               ptx::mma_ts_w(tmem + out + D, pk + ca, dod, idesc_o, acc);
               if constexpr (kSplit) ptx::mma_ts_w(tmem + out + D, pk + ca + 16, dod, idesc_o, 1u);
               ptx::mma_ts_w(tmem + out, pk + 64 + ca, qd, idesc_o, acc);
               if constexpr (kSplit) ptx::mma_ts_w(tmem + out, pk + 64 + ca + 16, qd, idesc_o, 1u);
             } else {
               // dQ += dS K (bf16: hi + lo), exact-D: PK += P K (same B operand)
-              const uint64_t kd = ptx::make_sdesc(b0 + boff, 128 * S::kRowBytes, kSbo, kSw);
+              const uint64_t kd = ptx::make_sdesc(b0 + boff, S::kBHalf, kSbo, kSw);
               ptx::mma_ts_w(tmem + out, pk + 64 + ca, kd, idesc_o, acc);
               if constexpr (kSplit) ptx::mma_ts_w(tmem + out, pk + 64 + ca + 16, kd, idesc_o, 1u);
               if constexpr (kExactD) ptx::mma_ts_w(tmem + out + D, pk + ca, kd, idesc_o, acc);
@@ -485,6 +512,11 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         store_ab = -1;
       }
     };
+    // Byte offset of 8-column chunk `ch` of this row in a staged stationary
+    // tile (head_dim 128: chunks 8..15 in the second half).
+    auto sto = [&](int ch) -> uint32_t {
+      return (uint32_t)(ch >> 3) * S::kAHalf + ptx::swz_off(row, ch & 7, S::kRowBytes);
+    };
     auto drain = [&](uint32_t src, uint8_t* stage, int col0, int ncols, float mul) {
       // 32 columns per TMEM round trip (two loads, one wait): the drain is
       // latency-bound on tcgen05.ld -> wait.
@@ -500,7 +532,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         const int chunk = (col0 + c0) / 8;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + q, S::kRowBytes)) =
+          *reinterpret_cast<uint4*>(stage + sto(chunk + q)) =
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
       }
       if (c0 + 8 == ncols) {  // an 8-column remainder (dQ halves at D = 16)
@@ -514,7 +546,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
 #pragma unroll
         for (int c = 0; c < 8; c += 2)
           pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
-        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, (col0 + c0) / 8, S::kRowBytes)) =
+        *reinterpret_cast<uint4*>(stage + sto((col0 + c0) / 8)) =
             make_uint4(pk[0], pk[1], pk[2], pk[3]);
       } else if (c0 < ncols) {  // a 16-column remainder (dQ halves at D = 32)
         uint32_t ov[16];
@@ -530,9 +562,9 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         for (int c = 0; c < 16; c += 2)
           pk[c >> 1] = pack2<BF16>(__uint_as_float(ov[c]) * mul, __uint_as_float(ov[c + 1]) * mul);
         const int chunk = (col0 + c0) / 8;
-        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk, S::kRowBytes)) =
+        *reinterpret_cast<uint4*>(stage + sto(chunk)) =
             make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + 1, S::kRowBytes)) =
+        *reinterpret_cast<uint4*>(stage + sto(chunk + 1)) =
             make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
     };
@@ -555,7 +587,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         for (int c = 0; c < 8; c += 2)
           pk[c >> 1] = pack2<BF16>((__uint_as_float(ov[c]) - corr * __uint_as_float(kv_[c])) * mul,
                                    (__uint_as_float(ov[c + 1]) - corr * __uint_as_float(kv_[c + 1])) * mul);
-        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, col0 / 8, S::kRowBytes)) =
+        *reinterpret_cast<uint4*>(stage + sto(col0 / 8)) =
             make_uint4(pk[0], pk[1], pk[2], pk[3]);
         return;
       }
@@ -570,9 +602,9 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           pk[c >> 1] = pack2<BF16>((__uint_as_float(ov[c]) - corr * __uint_as_float(kv_[c])) * mul,
                                    (__uint_as_float(ov[c + 1]) - corr * __uint_as_float(kv_[c + 1])) * mul);
         const int chunk = (col0 + c0) / 8;
-        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk, S::kRowBytes)) =
+        *reinterpret_cast<uint4*>(stage + sto(chunk)) =
             make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, chunk + 1, S::kRowBytes)) =
+        *reinterpret_cast<uint4*>(stage + sto(chunk + 1)) =
             make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
     };
@@ -592,7 +624,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       if (tracer) NA_TRACE_EV(2 + grp, tr, 24);
       ptx::tc_fence_after();
       uint8_t* stage0 = smem + S::kA + (2 * ab) * S::kTile;
-      const uint32_t src = kColOut + ob * kOutCols;
+      const uint32_t src = kColOut + ob * kOutCols;  // (kColOut: this D's layout, BwdTmem)
       if constexpr (KV_STATIONARY) {
         drain(src, stage0, 0, D, g.scale);                 // dK -> K tile
         drain(src + D, stage0 + S::kTile, 0, D, 1.f);      // dV -> V tile
@@ -623,12 +655,14 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
         }
       }
       if (store_now) {
-        for (int i = 0; i < pl.q_issues; ++i) {
-          t.template store_box<RANK>(&map_out0, stage0 + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
-          if constexpr (KV_STATIONARY)
-            t.template store_box<RANK>(&map_out1, stage0 + S::kTile + i * pl.q_box_x * S::kRowBytes,
-                                       i * pl.q_box_x, g);
-        }
+        for (int h = 0; h < S::kHalves; ++h)
+          for (int i = 0; i < pl.q_issues; ++i) {
+            t.template store_box<RANK>(&map_out0, stage0 + h * S::kAHalf + i * pl.q_box_x * S::kRowBytes,
+                                       i * pl.q_box_x, g, 64 * h);
+            if constexpr (KV_STATIONARY)
+              t.template store_box<RANK>(&map_out1, stage0 + S::kTile + h * S::kAHalf + i * pl.q_box_x * S::kRowBytes,
+                                         i * pl.q_box_x, g, 64 * h);
+          }
         ptx::bulk_commit();
         store_ab = ab;
       }
@@ -687,10 +721,10 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
             else if constexpr (!KV_STATIONARY) row_read(tn, rn, nrow_nl2, nrow_d);
           }
         }
-        const uint32_t b3 = gu % 3;
+        const uint32_t b3 = gu % kNB;
         const uint32_t buf = b3 * 128;  // S at +0, dP at +64; P / dS written back in place
         if (tracer) NA_TRACE_EV(2 + grp, tr, 19);
-        ptx::mbar_wait(bar + B_S + b3, (gu / 3) & 1);
+        ptx::mbar_wait(bar + B_S + b3, (gu / kNB) & 1);
         if constexpr (KV_STATIONARY) {
           // The chunk's stage is still held (its B_E needs this P), so its
           // phase is current: the row-vector bytes are visible after this.
@@ -905,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int RANK, int D, bool BF16, bool PRECISE = false>
 cudaError_t launch_all(int dtype, const Geom& g, const TcPlan* pls, const BwdMaps& mkv, const BwdMaps& mq,
                        const void* o, const void* d_o, float* rv, const float* lse, cudaStream_t st) {
-  constexpr bool kFuse = RANK == 1;  // dQ forms the row vectors (see bwd_body)
+  constexpr bool kFuse = RANK == 1 && D <= 64;  // dQ forms the row vectors (see bwd_body)
   const int smem_kv = BwdSmem<D, true, false>::kBytes + 1024;
   const int smem_q = BwdSmem<D, false, kFuse, BF16 && PRECISE>::kBytes + 1024;
   auto kdkdv = fna_dkdv_tc<RANK, D, BF16, PRECISE>;
@@ -941,6 +975,9 @@ cudaError_t by_type(int dtype, const Geom& g, const TcPlan* pl, const BwdMaps& m
                     const void* o, const void* d_o, float* rv, const float* lse, cudaStream_t st) {
   if (dtype == 2) {
     const bool pr = bf16_precise(g);
+    if (g.D == 128)
+      return pr ? launch_all<RANK, 128, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
+                : launch_all<RANK, 128, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
     if (g.D == 64)
       return pr ? launch_all<RANK, 64, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
                 : launch_all<RANK, 64, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
@@ -950,6 +987,7 @@ cudaError_t by_type(int dtype, const Geom& g, const TcPlan* pl, const BwdMaps& m
     return pr ? launch_all<RANK, 32, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
               : launch_all<RANK, 32, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
   }
+  if (g.D == 128) return launch_all<RANK, 128, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
   if (g.D == 64) return launch_all<RANK, 64, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
   if (g.D == 16) return launch_all<RANK, 16, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
   return launch_all<RANK, 32, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
@@ -985,7 +1023,7 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   mq.out1 = mq.out0;
   if ((e = make_map(&mq.o, dtype, g, o, pls[1].tq, pls[1].q_box_x)) != cudaSuccess) return e;
   mkv.o = mq.o;
-  *launches = g.rank == 1 ? 2 : 3;
+  *launches = (g.rank == 1 && g.D <= 64) ? 2 : 3;  // rank 1: preprocess fused into dQ (head_dim <= 64)
   switch (g.rank) {
     case 1: return by_type<1>(dtype, g, pls, mkv, mq, o, d_o, Dvec, lse, st);
     case 2: return by_type<2>(dtype, g, pls, mkv, mq, o, d_o, Dvec, lse, st);

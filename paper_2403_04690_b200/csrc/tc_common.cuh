@@ -173,16 +173,17 @@ struct TileCtx {
   // TMA load of a box whose compacted corner is `org` (+x_off on the
   // innermost axis).  Coordinates are original-tensor element coordinates
   // r + dil * c; the tensor map's elementStrides = dil walks the class.
+  // c0: first head_dim column (64 for the second half of a 128-wide row).
   template <int R>
   __device__ __forceinline__ void load_box(const CUtensorMap* m, void* dst, uint64_t* bar,
-                                           const int org[3], int x_off, const Geom& g) const {
+                                           const int org[3], int x_off, const Geom& g, int c0 = 0) const {
     if constexpr (R == 1) {
-      ptx::tma_load_3d_w(dst, m, bar, 0, r[0] + g.dil[0] * (org[0] + x_off), bh);
+      ptx::tma_load_3d_w(dst, m, bar, c0, r[0] + g.dil[0] * (org[0] + x_off), bh);
     } else if constexpr (R == 2) {
-      ptx::tma_load_4d_w(dst, m, bar, 0, r[1] + g.dil[1] * (org[1] + x_off),
+      ptx::tma_load_4d_w(dst, m, bar, c0, r[1] + g.dil[1] * (org[1] + x_off),
                        r[0] + g.dil[0] * org[0], bh);
     } else {
-      ptx::tma_load_5d_w(dst, m, bar, 0, r[2] + g.dil[2] * (org[2] + x_off),
+      ptx::tma_load_5d_w(dst, m, bar, c0, r[2] + g.dil[2] * (org[2] + x_off),
                        r[1] + g.dil[1] * org[1], r[0] + g.dil[0] * org[0], bh);
     }
   }
@@ -190,14 +191,14 @@ struct TileCtx {
   // TMA store of the stationary tile's box (one thread issues).
   template <int R>
   __device__ __forceinline__ void store_box(const CUtensorMap* m, const void* src, int x_off,
-                                            const Geom& g) const {
+                                            const Geom& g, int c0 = 0) const {
     if constexpr (R == 1) {
-      ptx::tma_store_3d(m, src, 0, r[0] + g.dil[0] * (q_origin[0] + x_off), bh);
+      ptx::tma_store_3d(m, src, c0, r[0] + g.dil[0] * (q_origin[0] + x_off), bh);
     } else if constexpr (R == 2) {
-      ptx::tma_store_4d(m, src, 0, r[1] + g.dil[1] * (q_origin[1] + x_off), r[0] + g.dil[0] * q_origin[0],
+      ptx::tma_store_4d(m, src, c0, r[1] + g.dil[1] * (q_origin[1] + x_off), r[0] + g.dil[0] * q_origin[0],
                         bh);
     } else {
-      ptx::tma_store_5d(m, src, 0, r[2] + g.dil[2] * (q_origin[2] + x_off), r[1] + g.dil[1] * q_origin[1],
+      ptx::tma_store_5d(m, src, c0, r[2] + g.dil[2] * (q_origin[2] + x_off), r[1] + g.dil[1] * q_origin[1],
                         r[0] + g.dil[0] * q_origin[0], bh);
     }
   }

@@ -48,7 +48,7 @@
 namespace na {
 namespace {
 
-constexpr int kStages = 2;
+constexpr int kMaxStages = 2;  // K/V ring depth bound (barrier slots); FwdSmem<D>::kStages is the depth
 constexpr int kThreads = 256;
 constexpr int kSoftmax = 128;    // softmax threads (warps 0..3)
 // The warp scheduler favours the highest warp id among eligible warps, so the
@@ -74,25 +74,40 @@ constexpr uint32_t kRegsOtherSmall = 40;
 // 16-bit pairs (A operand of PV); O [192, 192 + D) the fp32 accumulator.
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 constexpr uint32_t kColPSmall = 64, kColOSmall = 96;
-template <bool SMALL>
+// head_dim 128 (KV chunks <= 64 keys): S [0, 64), P [64, 96), O [128, 256).
+template <bool SMALL, bool WIDE = false>
 struct FwdCfg {
   static constexpr int kCtas = SMALL ? 3 : 2;            // CTAs per SM
   static constexpr uint32_t kTmemCols = SMALL ? 128 : 256;
-  static constexpr uint32_t kColP_ = SMALL ? kColPSmall : kColP;
-  static constexpr uint32_t kColO_ = SMALL ? kColOSmall : kColO;
-  static constexpr int kGroups = SMALL ? 2 : 4;          // 32-column groups of a round
+  static constexpr uint32_t kColP_ = SMALL ? kColPSmall : WIDE ? 64 : kColP;
+  static constexpr uint32_t kColO_ = SMALL ? kColOSmall : WIDE ? 128 : kColO;
+  static constexpr int kGroups = (SMALL || WIDE) ? 2 : 4;  // 32-column groups of a round
   static constexpr uint32_t kRegsS = SMALL ? kRegsSoftmaxSmall : kRegsSoftmax;
   static constexpr uint32_t kRegsO = SMALL ? kRegsOtherSmall : kRegsOther;
 };
 
+// head_dim 128 ("wide"): a 256-byte row exceeds the 128-byte swizzle span,
+// so every tile is stored as two 64-column halves [half][rows][128 B], each
+// a SW128 operand (TMA loads / stores one half per issue, c0 = 0 / 64); the
+// S MMA's K-steps 4..7 read the second halves, and V (the MN-major B of PV)
+// has its two 64-column atoms LBO = one half apart.  KV chunks hold <= 64
+// keys (planner) and the ring has one stage, so Q x 2 + K + V = 96 KB and
+// two CTAs still fit an SM.
 template <int D>
 struct FwdSmem {
-  static constexpr int kRowBytes = D * 2;
-  static constexpr int kTile = 128 * kRowBytes;  // Q tile, or one K/V stage
-  static constexpr int kQ = 0;                   // [2] (double-buffered across tiles)
+  static constexpr bool kWide = D > 64;
+  static constexpr int kHalves = kWide ? 2 : 1;
+  static constexpr int kRowBytes = (kWide ? 64 : D) * 2;  // one swizzled row (of one half)
+  static constexpr int kKvRows = kWide ? 64 : 128;        // K / V rows per stage
+  static constexpr int kStages = kWide ? 1 : 2;           // K / V ring depth
+  static constexpr int kQHalf = 128 * kRowBytes;
+  static constexpr int kTile = kHalves * kQHalf;          // Q tile (also the O staging tile)
+  static constexpr int kKvHalf = kKvRows * kRowBytes;
+  static constexpr int kKvTile = kHalves * kKvHalf;       // one K or V stage
+  static constexpr int kQ = 0;                            // [2] (double-buffered across tiles)
   static constexpr int kK = kQ + 2 * kTile;
-  static constexpr int kV = kK + kStages * kTile;
-  static constexpr int kBar = kV + kStages * kTile;
+  static constexpr int kV = kK + kStages * kKvTile;
+  static constexpr int kBar = kV + kStages * kKvTile;
   static constexpr int kBytes = kBar + 256;
 };
 
@@ -100,11 +115,11 @@ struct FwdSmem {
 enum : int {
   B_QF = 0,                 // Q buffer full [2]
   B_QE = B_QF + 2,          // Q buffer empty [2]
-  B_K = B_QE + 2,           // K stage full [kStages]
-  B_V = B_K + kStages,      // V stage full [kStages]
-  B_KE = B_V + kStages,     // K stage free (its S MMA is done) [kStages]
-  B_VE = B_KE + kStages,    // V stage free (its PV MMA is done) [kStages]
-  B_S = B_VE + kStages,     // S of a round ready
+  B_K = B_QE + 2,           // K stage full [kMaxStages]
+  B_V = B_K + kMaxStages,      // V stage full [kMaxStages]
+  B_KE = B_V + kMaxStages,     // K stage free (its S MMA is done) [kMaxStages]
+  B_VE = B_KE + kMaxStages,    // V stage free (its PV MMA is done) [kMaxStages]
+  B_S = B_VE + kMaxStages,     // S of a round ready
   B_SF = B_S + 1,           // S loaded by the softmax warps: buffer free (128 arrivals)
   B_P = B_SF + 1,           // P of a round written (128 arrivals)
   B_PF = B_P + 1,           // PV of a round done: P buffer free, O stable
@@ -129,7 +144,8 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
   const CUtensorMap& map_o = maps.o;
   using S = FwdSmem<D>;
   constexpr bool kSumRounded = BF16 && PRECISE;
-  using C = FwdCfg<SMALL>;
+  using C = FwdCfg<SMALL, (D > 64)>;
+  constexpr int kStages = S::kStages;
   constexpr uint32_t kColP = C::kColP_, kColO = C::kColO_;
   constexpr int kG = C::kGroups;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -148,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
     ptx::mbar_init(bar + B_OF, 1);
     ptx::mbar_init(bar + B_SF, kSoftmax);
     ptx::mbar_init(bar + B_PF, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       ptx::mbar_init(bar + B_K + s, 1);
       ptx::mbar_init(bar + B_V + s, 1);
       ptx::mbar_init(bar + B_KE + s, 1);
@@ -160,11 +176,11 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
   }
   // Zero the K/V rows no TMA box writes (rows_kv..127): the MMA reads up to
   // n_kv rows and 0 * garbage could be NaN.
-  if (pl.rows_kv < 128) {
-    const int nz = (128 - pl.rows_kv) * S::kRowBytes / 16;
-    for (int i = threadIdx.x; i < 2 * kStages * nz; i += kThreads) {
-      const int buf = i / nz, off = i % nz;
-      uint4* base = reinterpret_cast<uint4*>(smem + S::kK + buf * S::kTile + pl.rows_kv * S::kRowBytes);
+  if (pl.rows_kv < S::kKvRows) {
+    const int nz = (S::kKvRows - pl.rows_kv) * S::kRowBytes / 16;
+    for (int i = threadIdx.x; i < 2 * kStages * S::kHalves * nz; i += kThreads) {
+      const int buf = i / nz, off = i % nz;  // buf = (K or V stage) x half
+      uint4* base = reinterpret_cast<uint4*>(smem + S::kK + buf * S::kKvHalf + pl.rows_kv * S::kRowBytes);
       base[off] = make_uint4(0, 0, 0, 0);
     }
     ptx::fence_proxy_async();
@@ -182,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
     ptx::tma_prefetch(&map_q);
     ptx::tma_prefetch(&map_k);
     ptx::tma_prefetch(&map_v);
-    const uint32_t kv_bytes = pl.rows_kv * S::kRowBytes;
+    const uint32_t kv_bytes = pl.rows_kv * S::kRowBytes * S::kHalves;
     uint32_t kv_it = 0, ti = 0;
     int tr = 0;
     for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -190,26 +206,29 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
       if (!t.init(g, pl, tile)) continue;
       const int qb = ti & 1;
       if (ti >= 2) ptx::mbar_wait(bar + B_QE + qb, ((ti >> 1) - 1) & 1);
-      ptx::mbar_expect_tx_w(bar + B_QF + qb, 128 * S::kRowBytes);
-      for (int i = 0; i < pl.q_issues; ++i)
-        t.template load_box<RANK>(&map_q, smem + S::kQ + qb * S::kTile + i * pl.q_box_x * S::kRowBytes,
-                                  bar + B_QF + qb, t.q_origin, i * pl.q_box_x, g);
+      ptx::mbar_expect_tx_w(bar + B_QF + qb, S::kTile);
+      for (int h = 0; h < S::kHalves; ++h)
+        for (int i = 0; i < pl.q_issues; ++i)
+          t.template load_box<RANK>(&map_q, smem + S::kQ + qb * S::kTile + h * S::kQHalf + i * pl.q_box_x * S::kRowBytes,
+                                    bar + B_QF + qb, t.q_origin, i * pl.q_box_x, g, 64 * h);
       int org[3] = {t.lo[0], t.lo[1], t.lo[2]};
       for (int j = 0; j < t.nchunks; ++j, ++kv_it, t.next_origin(pl, org)) {
         const int s = kv_it % kStages;
         const uint32_t ph = ((kv_it / kStages) - 1) & 1;
-        uint8_t* kd = smem + S::kK + s * S::kTile;
-        uint8_t* vd = smem + S::kV + s * S::kTile;
+        uint8_t* kd = smem + S::kK + s * S::kKvTile;
+        uint8_t* vd = smem + S::kV + s * S::kKvTile;
         if (kv_it >= kStages) ptx::mbar_wait(bar + B_KE + s, ph);
         ptx::mbar_expect_tx_w(bar + B_K + s, kv_bytes);
-        for (int i = 0; i < pl.kv_issues; ++i)
-          t.template load_box<RANK>(&map_k, kd + i * pl.kv_box_x * S::kRowBytes, bar + B_K + s, org,
-                                    i * pl.kv_box_x, g);
+        for (int h = 0; h < S::kHalves; ++h)
+          for (int i = 0; i < pl.kv_issues; ++i)
+            t.template load_box<RANK>(&map_k, kd + h * S::kKvHalf + i * pl.kv_box_x * S::kRowBytes, bar + B_K + s,
+                                      org, i * pl.kv_box_x, g, 64 * h);
         if (kv_it >= kStages) ptx::mbar_wait(bar + B_VE + s, ph);
         ptx::mbar_expect_tx_w(bar + B_V + s, kv_bytes);
-        for (int i = 0; i < pl.kv_issues; ++i)
-          t.template load_box<RANK>(&map_v, vd + i * pl.kv_box_x * S::kRowBytes, bar + B_V + s, org,
-                                    i * pl.kv_box_x, g);
+        for (int h = 0; h < S::kHalves; ++h)
+          for (int i = 0; i < pl.kv_issues; ++i)
+            t.template load_box<RANK>(&map_v, vd + h * S::kKvHalf + i * pl.kv_box_x * S::kRowBytes, bar + B_V + s,
+                                      org, i * pl.kv_box_x, g, 64 * h);
         NA_TRACE_EV(0, tr, 1);
       }
       ++ti;
@@ -231,11 +250,13 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
       ptx::mbar_wait(bar + B_K + s, (kv / kStages) & 1);
       ptx::tc_fence_after();
       NA_TRACE_EV(1, tr, 10);
-      const uint32_t k_addr = ptx::smem_u32(smem + S::kK + s * S::kTile);
+      const uint32_t k_addr = ptx::smem_u32(smem + S::kK + s * S::kKvTile);
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk)
-        ptx::mma_ss_w(tmem + kColS, ptx::make_sdesc(q_addr + kk * 32, 16, kSbo, kSw),
-                      ptx::make_sdesc(k_addr + kk * 32, 16, kSbo, kSw), idesc_s, kk > 0);
+      for (int kk = 0; kk < D / 16; ++kk) {  // K-steps 4..7 (head_dim 128): second halves
+        const uint32_t hq = (kk >> 2) * S::kQHalf, hk = (kk >> 2) * S::kKvHalf, ko = (kk & 3) * 32;
+        ptx::mma_ss_w(tmem + kColS, ptx::make_sdesc(q_addr + hq + ko, 16, kSbo, kSw),
+                      ptx::make_sdesc(k_addr + hk + ko, 16, kSbo, kSw), idesc_s, kk > 0);
+      }
       ptx::mma_commit_w(bar + B_S);
       ptx::mma_commit_w(bar + B_KE + s);
     };
@@ -268,10 +289,10 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
         NA_TRACE_EV(1, tr, 11);
         ptx::mbar_wait(bar + B_V + s, (kv / kStages) & 1);
         ptx::tc_fence_after();
-        const uint32_t v_addr = ptx::smem_u32(smem + S::kV + s * S::kTile);
+        const uint32_t v_addr = ptx::smem_u32(smem + S::kV + s * S::kKvTile);
         for (int kk = 0; kk < kblocks; ++kk)  // O += P V, K-dim = keys
           ptx::mma_ts_w(tmem + kColO, tmem + kColP + kk * 8,
-                        ptx::make_sdesc(v_addr + kk * 16 * S::kRowBytes, 128 * S::kRowBytes, kSbo, kSw),
+                        ptx::make_sdesc(v_addr + kk * 16 * S::kRowBytes, S::kKvHalf, kSbo, kSw),
                         idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         ptx::mma_commit_w(bar + B_VE + s);  // V stage free after these MMAs
         ptx::mma_commit_w(bar + B_PF);      // P buffer free, O stable
@@ -451,7 +472,8 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < kEc; c += 8)
-          *reinterpret_cast<uint4*>(stage + ptx::swz_off(row, (c0 + c) / 8, S::kRowBytes)) =
+          *reinterpret_cast<uint4*>(stage + ((c0 + c) / 64) * S::kQHalf +
+                                    ptx::swz_off(row, ((c0 + c) / 8) & 7, S::kRowBytes)) =
               make_uint4(pack2<BF16>(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv),
                          pack2<BF16>(__uint_as_float(ov[c + 2]) * inv, __uint_as_float(ov[c + 3]) * inv),
                          pack2<BF16>(__uint_as_float(ov[c + 4]) * inv, __uint_as_float(ov[c + 5]) * inv),
@@ -464,8 +486,10 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
       ptx::fence_proxy_async();           // staged O visible to the TMA engine
       ptx::named_bar_sync(1, kSoftmax);
       if (threadIdx.x == 0) {
-        for (int i = 0; i < pl.q_issues; ++i)
-          t.template store_box<RANK>(&map_o, stage + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x, g);
+        for (int h = 0; h < S::kHalves; ++h)
+          for (int i = 0; i < pl.q_issues; ++i)
+            t.template store_box<RANK>(&map_o, stage + h * S::kQHalf + i * pl.q_box_x * S::kRowBytes, i * pl.q_box_x,
+                                       g, 64 * h);
         ptx::bulk_commit();
         ptx::bulk_wait_read<0>();
         ptx::mbar_arrive(bar + B_QE + qb);  // Q buffer reusable
@@ -490,6 +514,9 @@ template <int RANK, int D, bool BF16, bool PRECISE, bool SMALL>
 cudaError_t launch_v(const Geom& g, const TcPlan& pl, const FwdMaps& maps, float* lse, cudaStream_t st) {
   auto kern = fna_fwd_tc<RANK, D, BF16, PRECISE, SMALL>;
   const int smem = FwdSmem<D>::kBytes + 1024;
+  if constexpr (D > 64) {
+    if (pl.n_kv > FwdSmem<D>::kKvRows) return cudaErrorInvalidConfiguration;  // planner bound
+  }
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const long long tiles = (long long)g.BH * pl.nres * pl.tiles;
@@ -516,12 +543,15 @@ cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const FwdMaps& m
                     cudaStream_t st) {
   if (dtype == 2) {
     const bool pr = bf16_precise(g);
+    if (g.D == 128) return pr ? launch<RANK, 128, true, true>(g, pl, maps, lse, st)
+                              : launch<RANK, 128, true>(g, pl, maps, lse, st);
     if (g.D == 64) return pr ? launch<RANK, 64, true, true>(g, pl, maps, lse, st)
                              : launch<RANK, 64, true>(g, pl, maps, lse, st);
     if (g.D == 16) return pr ? launch<RANK, 16, true, true>(g, pl, maps, lse, st)
                              : launch<RANK, 16, true>(g, pl, maps, lse, st);
     return pr ? launch<RANK, 32, true, true>(g, pl, maps, lse, st) : launch<RANK, 32, true>(g, pl, maps, lse, st);
   }
+  if (g.D == 128) return launch<RANK, 128, false>(g, pl, maps, lse, st);
   if (g.D == 64) return launch<RANK, 64, false>(g, pl, maps, lse, st);
   if (g.D == 16) return launch<RANK, 16, false>(g, pl, maps, lse, st);
   return launch<RANK, 32, false>(g, pl, maps, lse, st);

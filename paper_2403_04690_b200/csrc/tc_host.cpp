@@ -20,7 +20,10 @@ namespace na {
 
 bool tc_supported(int dtype, const Geom& g, const char** why) {
   if (dtype != 1 && dtype != 2) { *why = "tensor-core path is fp16/bf16 only"; return false; }
-  if (g.D != 16 && g.D != 32 && g.D != 64) { *why = "tensor-core path needs head_dim 16, 32 or 64"; return false; }
+  if (g.D != 16 && g.D != 32 && g.D != 64 && g.D != 128) {
+    *why = "tensor-core path needs head_dim 16, 32, 64 or 128";
+    return false;
+  }
   for (int a = 0; a < g.rank; ++a) {
     if (g.dil[a] > 8) { *why = "TMA element strides limit dilation to <= 8"; return false; }
   }
@@ -66,11 +69,14 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand)
   pl.nres = 1;
   for (int a = 0; a < g.rank; ++a) pl.nres *= g.dil[a];
   if (ncand) *ncand = 1;
+  // head_dim 128: KV chunks of <= 64 keys (shared memory: two CTAs per SM
+  // forward, four streamed stages backward; tc_fwd.cu / tc_bwd.cu).
+  const int kv_max = g.D > 64 ? 64 : 128;
   if (g.rank == 1) {
     pl.tq[0] = tile_rows;
-    pl.ckv[0] = 128;
+    pl.ckv[0] = kv_max;
     pl.q_box_x = box_x_for(tile_rows, g.dil[0]);
-    pl.kv_box_x = box_x_for(128, g.dil[0]);
+    pl.kv_box_x = box_x_for(kv_max, g.dil[0]);
   } else {
     // Enumerate power-of-two query tiles (product tile_rows) and every KV
     // chunk box that tiles the tile's interior halo t + k - 1 per axis with
@@ -107,7 +113,7 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand)
         int last = -1;
         for (int n = 1; n <= h[a] && nopt[a] < 160; ++n) {
           const int c = ceil_div(h[a], n);
-          if (c == last || c > 128 || c * g.dil[a] > 256) continue;
+          if (c == last || c > kv_max || c * g.dil[a] > 256) continue;
           opts[a][nopt[a]++] = last = c;
         }
       }
@@ -116,7 +122,7 @@ TcPlan make_plan_uncached(const Geom& g, int tile_rows, int pick_in, int* ncand)
           for (int i2 = 0; i2 < nopt[2]; ++i2) {
             const int ck[3] = {opts[0][i0], opts[1][i1], opts[2][i2]};
             const int rows = ck[0] * ck[1] * ck[2];
-            if (rows > 128) continue;
+            if (rows > kv_max) continue;
             int chunks = 1;
             for (int a = 0; a < R; ++a) chunks *= ceil_div(h[a], ck[a]);
             const double cost = (double)chunks * (round16(rows) + kRoundCols) / valid_rows;
@@ -249,7 +255,7 @@ TcPlan make_plan(const Geom& g, int tile_rows, int pick, int* ncand) {
   int key[16];
   geom_key(g, tile_rows, key);
   key[14] = pick;
-  key[15] = g.D <= 32;  // the candidate list depends on it (small-chunk plan)
+  key[15] = g.D <= 32 ? 1 : g.D > 64 ? 2 : 0;  // the candidates depend on it (chunk limits)
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (const PlanEntry& e : g_plans)
@@ -403,7 +409,7 @@ cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* b
   cuuint32_t boxd[5], estr[5];
   const cuuint64_t row = (cuuint64_t)g.D * 2;
   dims[0] = g.D;
-  boxd[0] = g.D;
+  boxd[0] = g.D > 64 ? 64 : g.D;  // head_dim 128: two 64-column boxes per row (SW128 span)
   estr[0] = 1;
   for (int i = 1; i <= R; ++i) {
     const int a = R - i;
@@ -417,7 +423,7 @@ cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* b
   strides[R] = row * g.N;
   boxd[R + 1] = 1;
   estr[R + 1] = 1;
-  const CUtensorMapSwizzle sw = g.D == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+  const CUtensorMapSwizzle sw = g.D >= 64   ? CU_TENSOR_MAP_SWIZZLE_128B
                                : g.D == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                            : CU_TENSOR_MAP_SWIZZLE_32B;
   CUresult r = enc(map, dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,

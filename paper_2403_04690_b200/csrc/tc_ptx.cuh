@@ -182,7 +182,8 @@ __device__ __forceinline__ uint32_t swz_off(uint32_t row, uint32_t chunk, uint32
 }
 // Shared-memory descriptor layout code of the swizzle a D-wide 16-bit row uses
 // (2 = SW128, 4 = SW64, 6 = SW32).
-__host__ __device__ constexpr uint32_t sw_layout(int D) { return D == 64 ? 2u : D == 32 ? 4u : 6u; }
+// head_dim 128 rows are stored as two 64-column SW128 halves.
+__host__ __device__ constexpr uint32_t sw_layout(int D) { return D >= 64 ? 2u : D == 32 ? 4u : 6u; }
 
 // ------------------------------------------------------------------- tcgen05
 template <int NCOLS>

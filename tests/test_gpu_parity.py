@@ -70,7 +70,7 @@ SMALL = [
 
 
 def small_cases():
-    for (ext, ker, dil, cau), D, dt in itertools.product(SMALL, [16, 32, 64],
+    for (ext, ker, dil, cau), D, dt in itertools.product(SMALL, [16, 32, 64, 128],
                                                           [torch.float16, torch.bfloat16]):
         yield pytest.param(ext, ker, dil, cau, D, dt, id=f"{ext}-k{ker}-d{dil}-c{cau}-D{D}-{str(dt)[6:]}")
     for ext, ker, dil, cau in SMALL[::3]:
@@ -276,6 +276,7 @@ def test_baseline_config_full_slices(na, name):
 PLAN_CASES = [
     ([16, 12, 12], [7, 7, 7], [1, 1, 1], [1, 0, 0], 64, torch.float16),
     ([30, 44], [9, 13], [3, 2], [0, 1], 32, torch.bfloat16),
+    ([12, 14, 20], [5, 5, 7], [1, 2, 1], [0, 0, 1], 128, torch.float16),
 ]
 
 
@@ -308,7 +309,7 @@ def test_every_candidate_plan_matches_oracle(na, ext, ker, dil, cau, D, dt):
 
 # ------------------------------------------------------- randomized sweep
 
-def _random_cases(n=24, seed=2024):
+def _random_cases(n=24, seed=2024, dims=(16, 32, 64)):
     rng = np.random.default_rng(seed)
     out = []
     while len(out) < n:
@@ -325,13 +326,13 @@ def _random_cases(n=24, seed=2024):
             if k < 1:
                 k = 1
             ext.append(L), ker.append(k), dil.append(d), cau.append(c)
-        D = int(rng.choice([16, 32, 64]))
+        D = int(rng.choice(list(dims)))
         dt = [torch.float16, torch.bfloat16][int(rng.integers(0, 2))]
         out.append((ext, ker, dil, cau, D, dt))
     return out
 
 
-@pytest.mark.parametrize("ext,ker,dil,cau,D,dt", _random_cases(64))
+@pytest.mark.parametrize("ext,ker,dil,cau,D,dt", _random_cases(64) + _random_cases(24, seed=128, dims=(128,)))
 def test_random_problems_match_oracle(na, ext, ker, dil, cau, D, dt):
     """Seeded random shapes, windows, dilations, causal mixes, head dims and
     dtypes on the tensor-core path (planner, masks, halos, ragged classes)."""
