@@ -76,7 +76,8 @@ typedef enum {
 /* Kernel family selection (tests and benchmarks use it to pin a path). */
 /* Kernel family selection.  There is no silent fallback: with NA_IMPL_AUTO a
  * 16-bit problem runs on the tensor cores, and a 16-bit problem outside that
- * path (tc_supported: head_dim or dilation limits) fails with NA_ERR_IMPL
+ * path (tc_supported: head_dim not in {16, 32, 64, 128}, or a dilation
+ * above 8) fails with NA_ERR_IMPL
  * unless the caller selects NA_IMPL_SIMT explicitly.  fp32 inputs always run
  * on the CUDA-core kernels (TF32 off, north_star's 1e-4 bound). */
 typedef enum {
