@@ -21,11 +21,13 @@
  *   writer per element (no atomics).
  *
  * Conventions (all entry points):
- *   - Tensors Q, K, V, O, dO, dQ, dK, dV are DEVICE pointers to contiguous
+ *   - Tensors Q, K, V, O, dO, dQ, dK, dV are DEVICE pointers to
  *     [batch, heads, X0 (, X1 (, X2)), head_dim] arrays of `dtype`
- *     (X0 outermost; e.g. T, H, W for video).  LSE is a device pointer to a
- *     contiguous fp32 [batch, heads, X0 (, X1 (, X2))] array.  All base
- *     pointers must be 16-byte aligned.
+ *     (X0 outermost; e.g. T, H, W for video): contiguous when
+ *     na_problem.strides is NULL, else all eight share those element strides
+ *     (see na_problem).  LSE is a device pointer to a contiguous fp32
+ *     [batch, heads, X0 (, X1 (, X2))] array.  All base pointers must be
+ *     16-byte aligned.
  *   - The caller owns every buffer; the library never allocates device
  *     memory.  The backward workspace is caller-supplied.
  *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t;
@@ -66,8 +68,8 @@ typedef enum {
                                  in the smallest residue class  */
   NA_ERR_DTYPE = 8,           /* dtype not one of na_dtype                                 */
   NA_ERR_HEAD_DIM = 9,        /* head_dim > 256 or not a multiple of 8 (16-bit) / 4 (fp32) */
-  NA_ERR_ALIGNMENT = 10,      /* a tensor base pointer is not 16-byte aligned              */
-  NA_ERR_LAYOUT = 11,         /* non-contiguous strides requested (not supported)          */
+  NA_ERR_ALIGNMENT = 10,      /* a base pointer or a stride is not a 16-byte multiple      */
+  NA_ERR_LAYOUT = 11,         /* strides: head_dim stride != 1 or a stride < 1             */
   NA_ERR_WORKSPACE = 12,      /* backward workspace missing or smaller than required       */
   NA_ERR_CUDA = 13,           /* CUDA launch/driver error (see na_last_error)              */
   NA_ERR_IMPL = 14            /* the requested `impl` cannot run this problem              */
@@ -97,7 +99,16 @@ typedef struct {
   float scale;             /* softmax scale; <= 0 means 1/sqrt(head_dim)  */
   na_dtype dtype;          /* of Q,K,V,O,dO,dQ,dK,dV; LSE/workspace always fp32   */
   na_impl impl;            /* NA_IMPL_AUTO unless pinning a kernel family         */
-  const int64_t* strides;  /* must be NULL (contiguous); else NA_ERR_LAYOUT       */
+  /* NULL: contiguous [B, H, X0 (, X1 (, X2)), D].  Else 6 element strides
+   * {B, H, X0, X1, X2, D} shared by Q, K, V, O, dO, dQ, dK, dV (X_a with
+   * a >= rank ignored): D's must be 1, the others >= 1 and multiples of 16
+   * bytes (the tensor-core path addresses rows through TMA tensor maps).
+   * E.g. heads-last [B, X..., H, D] storage viewed as [B, H, X..., D], or
+   * one slice of a packed [B, X..., 3, H, D] QKV buffer.  When the batch
+   * stride is not heads x the head stride, each batch entry runs as its own
+   * launch set on the same stream (na_last_launch_count counts them all).
+   * The caller guarantees that output rows do not overlap. */
+  const int64_t* strides;
 } na_problem;
 
 /* Validates `p` alone (no pointers).  Pure host function; never touches a GPU. */

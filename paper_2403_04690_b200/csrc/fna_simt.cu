@@ -69,6 +69,17 @@ __device__ __forceinline__ int token_of(const Geom& g, const Coord& co, const in
   return t;
 }
 
+// Element offset, inside its (b, h) slice, of the token at compacted
+// coordinates cc of co's residue class (Geom::sX strides; contiguous:
+// token_of * D).
+__device__ __forceinline__ long long elem_of(const Geom& g, const Coord& co, const int cc[3]) {
+  long long e = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (a < g.rank) e += (long long)(co.r[a] + g.dil[a] * cc[a]) * g.sX[a];
+  return e;
+}
+
 // ------------------------------------------------------------------ forward
 template <typename T, int DPL>
 __global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict__ q,
@@ -79,15 +90,16 @@ __global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict_
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   const int bh = (int)(row / g.N), x = (int)(row % g.N);
-  const int64_t base = (int64_t)bh * g.N * g.D;
+  const int64_t base = (int64_t)bh * g.sBH;
+  const Coord co = decode(g, x);
+  const int64_t xe = base + elem_of(g, co, co.c);  // this query's row
   float qr[DPL], acc[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
     int d = lane + 32 * i;
-    qr[i] = d < g.D ? ld(q + base + (int64_t)x * g.D + d) * g.scale_log2 : 0.f;
+    qr[i] = d < g.D ? ld(q + xe + d) * g.scale_log2 : 0.f;
     acc[i] = 0.f;
   }
-  const Coord co = decode(g, x);
   int lo[3], hi[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -99,7 +111,7 @@ __global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict_
   for (cc[0] = lo[0]; cc[0] <= hi[0]; ++cc[0])
     for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
       for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
-        const int64_t y = base + (int64_t)token_of(g, co, cc) * g.D;
+        const int64_t y = base + elem_of(g, co, cc);
         float s = 0.f;
 #pragma unroll
         for (int i = 0; i < DPL; ++i) {
@@ -122,7 +134,7 @@ __global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict_
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
     int d = lane + 32 * i;
-    if (d < g.D) o[base + (int64_t)x * g.D + d] = cvt<T>(acc[i] * inv);
+    if (d < g.D) o[xe + d] = cvt<T>(acc[i] * inv);
   }
   if (lse && lane == 0) lse[row] = (m + log2f(l)) * 0.69314718055994531f;
 }
@@ -136,7 +148,8 @@ __global__ void __launch_bounds__(256) fna_bwd_pre(Geom g, const T* __restrict__
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   float s = 0.f;
-  for (int d = lane; d < g.D; d += 32) s = fmaf(ld(o + row * g.D + d), ld(d_o + row * g.D + d), s);
+  const int64_t re = elem_of_token(g, (int)(row / g.N), (int)(row % g.N));
+  for (int d = lane; d < g.D; d += 32) s = fmaf(ld(o + re + d), ld(d_o + re + d), s);
   s = warp_sum(s);
   if (lane == 0) Dvec[row] = s;
 }
@@ -154,6 +167,24 @@ __global__ void __launch_bounds__(256) fna_bwd_pre(Geom g, const T* __restrict__
 struct RvDiv {
   FastDiv n, l[3], dil[3];
 };
+
+// Element offset of row `row` (= bh * N + token) in a Q/K/V/O-type tensor
+// (Geom::sBH / sX strides), with the same fast divisions.
+__device__ __forceinline__ long long row_elem(const Geom& g, const RvDiv& f, long long row) {
+  const uint32_t r32 = (uint32_t)row;
+  const uint32_t bh = fdiv(r32, f.n);
+  uint32_t n = r32 - bh * f.n.d;
+  long long off = (long long)bh * g.sBH;
+#pragma unroll
+  for (int a = 2; a >= 0; --a) {
+    if (a < g.rank) {
+      const uint32_t rest = fdiv(n, f.l[a]);
+      off += (long long)(n - rest * f.l[a].d) * g.sX[a];
+      n = rest;
+    }
+  }
+  return off;
+}
 
 __device__ __forceinline__ long long rv_index(const Geom& g, const RvDiv& f, long long row) {
   // B*H*N < 2^31 for any problem whose tensors fit in memory (validated).
@@ -208,8 +239,9 @@ __global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restri
       l[k] = lse[row];
       i[k] = rv_index(g, f, row);
     }
-    a[k] = valid ? __ldg(reinterpret_cast<const uint4*>(o + row * g.D) + part) : make_uint4(0, 0, 0, 0);
-    b[k] = valid ? __ldg(reinterpret_cast<const uint4*>(d_o + row * g.D) + part) : make_uint4(0, 0, 0, 0);
+    const long long re = g.contig ? row * g.D : (valid ? row_elem(g, f, row) : 0);
+    a[k] = valid ? __ldg(reinterpret_cast<const uint4*>(o + re) + part) : make_uint4(0, 0, 0, 0);
+    b[k] = valid ? __ldg(reinterpret_cast<const uint4*>(d_o + re) + part) : make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
   for (int k = 0; k < kPreRows; ++k) {
@@ -250,18 +282,19 @@ __global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   const int bh = (int)(row / g.N), x = (int)(row % g.N);
-  const int64_t base = (int64_t)bh * g.N * g.D;
+  const int64_t base = (int64_t)bh * g.sBH;
+  const Coord co = decode(g, x);
+  const int64_t xe = base + elem_of(g, co, co.c);  // this query's row
   float qr[DPL], dor[DPL], acc[DPL], pk[DPL];
   float csum = 0.f;
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
     int d = lane + 32 * i;
-    qr[i] = d < g.D ? ld(q + base + (int64_t)x * g.D + d) : 0.f;
-    dor[i] = d < g.D ? ld(d_o + base + (int64_t)x * g.D + d) : 0.f;
+    qr[i] = d < g.D ? ld(q + xe + d) : 0.f;
+    dor[i] = d < g.D ? ld(d_o + xe + d) : 0.f;
     acc[i] = pk[i] = 0.f;
   }
   const float lse_x = lse[row], D_x = Dvec[row];
-  const Coord co = decode(g, x);
   int lo[3], hi[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -272,7 +305,7 @@ __global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__
   for (cc[0] = lo[0]; cc[0] <= hi[0]; ++cc[0])
     for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
       for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
-        const int64_t y = base + (int64_t)token_of(g, co, cc) * g.D;
+        const int64_t y = base + elem_of(g, co, cc);
         float s = 0.f, dp = 0.f;
 #pragma unroll
         for (int i = 0; i < DPL; ++i) {
@@ -300,7 +333,7 @@ __global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
     int d = lane + 32 * i;
-    if (d < g.D) dq[base + (int64_t)x * g.D + d] = cvt<T>((acc[i] - csum * pk[i]) * g.scale);
+    if (d < g.D) dq[xe + d] = cvt<T>((acc[i] - csum * pk[i]) * g.scale);
   }
   if (kCorr && lane == 0) Dvec[row] = D_x + csum;
 }
@@ -318,16 +351,17 @@ __global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, const T* __restrict
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   const int bh = (int)(row / g.N), y = (int)(row % g.N);
-  const int64_t base = (int64_t)bh * g.N * g.D;
+  const int64_t base = (int64_t)bh * g.sBH;
+  const Coord co = decode(g, y);
+  const int64_t ye = base + elem_of(g, co, co.c);  // this key's row
   float kr[DPL], vr[DPL], ak[DPL], av[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
     int d = lane + 32 * i;
-    kr[i] = d < g.D ? ld(k + base + (int64_t)y * g.D + d) : 0.f;
-    vr[i] = d < g.D ? ld(v + base + (int64_t)y * g.D + d) : 0.f;
+    kr[i] = d < g.D ? ld(k + ye + d) : 0.f;
+    vr[i] = d < g.D ? ld(v + ye + d) : 0.f;
     ak[i] = av[i] = 0.f;
   }
-  const Coord co = decode(g, y);
   int lo[3], hi[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {   // inverse neighborhood: exact per-axis intervals
@@ -339,7 +373,7 @@ __global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, const T* __restrict
     for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
       for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
         const int xt = token_of(g, co, cc);
-        const int64_t xo = base + (int64_t)xt * g.D;
+        const int64_t xo = base + elem_of(g, co, cc);
         float s = 0.f, dp = 0.f;
 #pragma unroll
         for (int i = 0; i < DPL; ++i) {
@@ -367,8 +401,8 @@ __global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, const T* __restrict
   for (int i = 0; i < DPL; ++i) {
     int d = lane + 32 * i;
     if (d < g.D) {
-      dk[base + (int64_t)y * g.D + d] = cvt<T>(ak[i] * g.scale);
-      dv[base + (int64_t)y * g.D + d] = cvt<T>(av[i]);
+      dk[ye + d] = cvt<T>(ak[i] * g.scale);
+      dv[ye + d] = cvt<T>(av[i]);
     }
   }
 }

@@ -65,7 +65,19 @@ na_status validate(const na_problem* p) {
   if (p->head_dim > 256 || p->head_dim % align)
     return fail(NA_ERR_HEAD_DIM, "head_dim %d: need <= 256 and a multiple of %d", p->head_dim,
                 align);
-  if (p->strides) return fail(NA_ERR_LAYOUT, "only contiguous [B,H,X...,D] is supported");
+  if (p->strides) {
+    // [B, H, X0, X1, X2, D] element strides; entries X_a for a >= rank ignored.
+    const int64_t* st = p->strides;
+    if (st[5] != 1) return fail(NA_ERR_LAYOUT, "head_dim stride must be 1 (got %lld)", (long long)st[5]);
+    const int esz = p->dtype == NA_F32 ? 4 : 2;
+    for (int i = 0; i < 5; ++i) {
+      if (i >= 2 && i - 2 >= p->rank) continue;
+      if (st[i] < 1) return fail(NA_ERR_LAYOUT, "stride[%d] = %lld < 1", i, (long long)st[i]);
+      if ((st[i] * esz) % 16)
+        return fail(NA_ERR_ALIGNMENT, "stride[%d] = %lld elements is not a multiple of 16 bytes", i,
+                    (long long)st[i]);
+    }
+  }
   if ((int64_t)p->batch * p->heads * n * p->head_dim > (int64_t(1) << 40))
     return fail(NA_ERR_SHAPE, "problem too large");
   if ((int64_t)p->batch * p->heads > 0x7fffffff || n > 0x7fffffff)
@@ -100,6 +112,17 @@ na::Geom make_geom(const na_problem* p) {
     s *= g.L[a];
   }
   for (int a = p->rank; a < 3; ++a) g.tstride[a] = 1;
+  for (int a = 0; a < 3; ++a) g.sX[a] = a < p->rank ? (long long)g.tstride[a] * g.D : 0;
+  g.sBH = (long long)n * g.D;
+  g.contig = 1;
+  if (p->strides) {
+    g.contig = 0;
+    for (int a = 0; a < p->rank; ++a) g.sX[a] = p->strides[2 + a];
+    // B and H merge into one slice index when stride_B = H * stride_H; the
+    // ABI calls split other layouts into one launch set per batch entry
+    // (split_batches), each with B = 1, where sBH = stride_H.
+    g.sBH = p->heads > 1 ? p->strides[1] : p->strides[0];
+  }
   g.scale = p->scale > 0.f ? p->scale : 1.f / std::sqrt((float)p->head_dim);
   g.scale_log2 = g.scale * 1.4426950408889634f;
   g.nres = 1;
@@ -143,6 +166,20 @@ int select_impl(const na_problem* p, const na::Geom& g, const char** why) {
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+
+// Strided layouts whose batch and head strides do not merge into one slice
+// index (stride_B != H * stride_H, e.g. heads-last [B, X..., H, D] views):
+// every batch entry is run as its own B = 1 problem on the same stream
+// (base pointers advanced by stride_B; LSE by H*N; the backward workspace
+// is reused, each sub-call consuming its row vectors before the next
+// writes them).
+bool split_batches(const na_problem* p) {
+  return p->strides && p->batch > 1 && p->heads > 1 && p->strides[0] != (int64_t)p->heads * p->strides[1];
+}
+const void* adv(const void* ptr, long long elems, int esz) {
+  return static_cast<const char*>(ptr) + elems * esz;
+}
+void* adv(void* ptr, long long elems, int esz) { return static_cast<char*>(ptr) + elems * esz; }
 
 na_status cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return NA_OK;
@@ -233,9 +270,21 @@ na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* 
     return fail(NA_ERR_IMPL, "tensor-core path cannot run this problem: %s (impl=NA_IMPL_SIMT selects the "
                 "CUDA-core kernels explicitly)", why);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  int launches = 1;
-  cudaError_t e = impl == NA_IMPL_TC ? na::tc_fwd((int)p->dtype, g, q, k, v, o, lse, st, &launches)
-                                     : na::simt_fwd((int)p->dtype, g, q, k, v, o, lse, st);
+  int launches = 1, total = 0;
+  const int nb = split_batches(p) ? p->batch : 1;
+  if (nb > 1) g.BH = p->heads;
+  const int esz = p->dtype == NA_F32 ? 4 : 2;
+  cudaError_t e = cudaSuccess;
+  for (int b = 0; b < nb && e == cudaSuccess; ++b) {
+    const long long eo = (long long)b * (nb > 1 ? p->strides[0] : 0);
+    const void *qb = adv(q, eo, esz), *kb = adv(k, eo, esz), *vb = adv(v, eo, esz);
+    void* ob = adv(o, eo, esz);
+    float* lb = lse ? lse + (long long)b * (nb > 1 ? (long long)g.BH * g.N : 0) : nullptr;
+    e = impl == NA_IMPL_TC ? na::tc_fwd((int)p->dtype, g, qb, kb, vb, ob, lb, st, &launches)
+                           : na::simt_fwd((int)p->dtype, g, qb, kb, vb, ob, lb, st);
+    total += launches;
+  }
+  launches = total;
   s = cuda_status(e, "na_fwd launch");
   if (s == NA_OK) {
     g_last_error.clear();
@@ -270,12 +319,24 @@ na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* 
     return fail(NA_ERR_IMPL, "tensor-core path cannot run this problem: %s (impl=NA_IMPL_SIMT selects the "
                 "CUDA-core kernels explicitly)", why);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  int launches = 3;
-  cudaError_t e =
-      impl == NA_IMPL_TC
-          ? na::tc_bwd((int)p->dtype, g, q, k, v, o, d_o, lse, dq, dk, dv, (float*)workspace, st,
-                       &launches)
-          : na::simt_bwd((int)p->dtype, g, q, k, v, o, d_o, lse, dq, dk, dv, (float*)workspace, st);
+  int launches = 3, total = 0;
+  const int nb = split_batches(p) ? p->batch : 1;
+  if (nb > 1) g.BH = p->heads;
+  const int esz = p->dtype == NA_F32 ? 4 : 2;
+  cudaError_t e = cudaSuccess;
+  for (int b = 0; b < nb && e == cudaSuccess; ++b) {
+    const long long eo = (long long)b * (nb > 1 ? p->strides[0] : 0);
+    const float* lb = lse + (long long)b * (nb > 1 ? (long long)g.BH * g.N : 0);
+    e = impl == NA_IMPL_TC
+            ? na::tc_bwd((int)p->dtype, g, adv(q, eo, esz), adv(k, eo, esz), adv(v, eo, esz), adv(o, eo, esz),
+                         adv(d_o, eo, esz), lb, adv(dq, eo, esz), adv(dk, eo, esz), adv(dv, eo, esz),
+                         (float*)workspace, st, &launches)
+            : na::simt_bwd((int)p->dtype, g, adv(q, eo, esz), adv(k, eo, esz), adv(v, eo, esz),
+                           adv(o, eo, esz), adv(d_o, eo, esz), lb, adv(dq, eo, esz), adv(dk, eo, esz),
+                           adv(dv, eo, esz), (float*)workspace, st);
+    total += launches;
+  }
+  launches = total;
   s = cuda_status(e, "na_bwd launch");
   if (s == NA_OK) {
     g_last_error.clear();

@@ -62,6 +62,12 @@ struct Geom {
   int D;           // head dim
   int L[3], k[3], dil[3], causal[3];  // padded with (1, 1, 1, 0) beyond rank
   int tstride[3];  // token stride of each axis in the flat spatial index
+  // Element strides of the 16-bit / fp32 tensors (head_dim stride 1): from
+  // one (b, h) slice to the next, and per spatial axis (padded with 0).
+  // Contiguous [B,H,X...,D]: sBH = N*D, sX[a] = tstride[a]*D.  LSE, the
+  // row vectors and the workspace are always contiguous.
+  long long sBH, sX[3];
+  int contig;  // 1: the contiguous layout (sBH = N*D, sX[a] = tstride[a]*D)
   float scale;     // softmax scale
   float scale_log2;  // scale * log2(e)
   // Backward row-vector layout (tensor-core path): per (b,h) and residue
@@ -73,6 +79,14 @@ struct Geom {
   int rv_cs[3];      // element stride per compacted axis
   long long rv_plane;  // elements per plane = rv_cs[0] * rv_lc[0]
 };
+
+// Element offset of flat token `tok` of slice `bh` in a Q/K/V/O-type tensor
+// (the token's coordinate on axis a is (tok / tstride[a]) % L[a]).
+NA_HD long long elem_of_token(const Geom& g, int bh, int tok) {
+  long long off = (long long)bh * g.sBH;
+  for (int a = 0; a < g.rank; ++a) off += (long long)((tok / g.tstride[a]) % g.L[a]) * g.sX[a];
+  return off;
+}
 
 // Offset of plane 0 of class `res` of head `bh` in the row-vector layout.
 NA_HD long long rv_base(const Geom& g, int bh, int res) {

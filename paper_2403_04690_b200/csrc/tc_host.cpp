@@ -407,20 +407,19 @@ cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* b
   const int R = g.rank;
   cuuint64_t dims[5], strides[4];
   cuuint32_t boxd[5], estr[5];
-  const cuuint64_t row = (cuuint64_t)g.D * 2;
   dims[0] = g.D;
   boxd[0] = g.D > 64 ? 64 : g.D;  // head_dim 128: two 64-column boxes per row (SW128 span)
   estr[0] = 1;
   for (int i = 1; i <= R; ++i) {
     const int a = R - i;
     dims[i] = g.L[a];
-    strides[i - 1] = row * g.tstride[a];
+    strides[i - 1] = (cuuint64_t)g.sX[a] * 2;  // element strides (contiguous: tstride * D)
     const int b = (i == 1) ? box_x : box[a];
     boxd[i] = (cuuint32_t)(b * g.dil[a]);
     estr[i] = g.dil[a];
   }
   dims[R + 1] = g.BH;
-  strides[R] = row * g.N;
+  strides[R] = (cuuint64_t)g.sBH * 2;
   boxd[R + 1] = 1;
   estr[R + 1] = 1;
   const CUtensorMapSwizzle sw = g.D >= 64   ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -442,17 +441,17 @@ cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* b
 cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base, const int box[3],
                      int box_x) {
   struct Entry {
-    int key[14];
+    long long key[18];
     const void* base;
     CUtensorMap map;
   };
   constexpr int kEntries = 64;
   thread_local Entry cache[kEntries];
   thread_local int used = 0, next = 0;
-  const int key[14] = {dtype, g.rank, g.D, g.BH, box_x, g.L[0], g.L[1], g.L[2], g.dil[0], g.dil[1], g.dil[2],
-                       box[0], box[1], box[2]};
+  const long long key[18] = {dtype, g.rank, g.D, g.BH, box_x, g.L[0], g.L[1], g.L[2], g.dil[0], g.dil[1], g.dil[2],
+                       box[0], box[1], box[2], g.sBH, g.sX[0], g.sX[1], g.sX[2]};
   for (int i = 0; i < used; ++i)
-    if (cache[i].base == base && std::equal(key, key + 14, cache[i].key)) {
+    if (cache[i].base == base && std::equal(key, key + 18, cache[i].key)) {
       *map = cache[i].map;
       return cudaSuccess;
     }
@@ -461,7 +460,7 @@ cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* bas
   Entry& en = cache[next];
   next = (next + 1) % kEntries;
   if (used < kEntries) ++used;
-  std::copy(key, key + 14, en.key);
+  std::copy(key, key + 18, en.key);
   en.base = base;
   en.map = *map;
   return cudaSuccess;

@@ -1,8 +1,12 @@
 """ctypes binding of include/na.h — argument marshalling only.
 
 Every step of the computation runs in libna.so's CUDA kernels.  Tensors are
-torch CUDA tensors in the ABI layout [B, H, X0 (, X1 (, X2)), D]; the call is
-enqueued on torch's current CUDA stream.
+torch CUDA tensors indexed [B, H, X0 (, X1 (, X2)), D]; a non-contiguous
+layout (e.g. a heads-last [B, X..., H, D] tensor viewed with permute) is
+passed to the ABI as element strides, so all tensors of one call must share
+q's strides (outputs are allocated with them).  LSE is always a contiguous
+fp32 [B, H, X...] tensor.  The call is enqueued on torch's current CUDA
+stream.
 """
 from __future__ import annotations
 
@@ -128,7 +132,18 @@ def _problem_from(q: torch.Tensor, kernel_size, dilation, is_causal, scale, impl
     if q.dim() < 4 or q.dim() > 6:
         raise ValueError("expected [B, H, X0 (, X1 (, X2)), D]")
     B, H, *ext, D = q.shape
-    return make_problem(B, H, ext, D, kernel_size, dilation, is_causal, scale, q.dtype, impl)
+    p = make_problem(B, H, ext, D, kernel_size, dilation, is_causal, scale, q.dtype, impl)
+    if not q.is_contiguous():  # na_problem.strides: [B, H, X0, X1, X2, D] in elements
+        sB, sH, *sX, sD = q.stride()
+        p._strides = (ctypes.c_int64 * 6)(sB, sH, *(list(sX) + [0] * (3 - len(sX))), sD)
+        p.strides = ctypes.cast(p._strides, ctypes.c_void_p)
+    return p
+
+
+def _like(q: torch.Tensor) -> torch.Tensor:
+    """An output with q's shape, dtype, device and strides."""
+    return torch.empty_like(q) if q.is_contiguous() else \
+        torch.empty_strided(q.shape, q.stride(), dtype=q.dtype, device=q.device)
 
 
 def _ptr(t):
@@ -155,9 +170,9 @@ def _need_cuda(q: torch.Tensor):
 
 def _need(t: torch.Tensor, like: torch.Tensor, name: str):
     if t.device != like.device or t.dtype != like.dtype or t.shape != like.shape or \
-            not t.is_contiguous():
-        raise ValueError(f"{name} must be a contiguous {like.dtype} tensor of shape "
-                         f"{tuple(like.shape)} on {like.device}")
+            t.stride() != like.stride():
+        raise ValueError(f"{name} must be a {like.dtype} tensor of shape {tuple(like.shape)} "
+                         f"and strides {like.stride()} (q's) on {like.device}")
 
 
 def na_validate(p: Problem) -> int:
@@ -203,7 +218,7 @@ def na_fwd(q, k, v, kernel_size, dilation=None, is_causal=None, scale=None, impl
     for t, n in ((q, "q"), (k, "k"), (v, "v")):
         _need(t, q, n)
     with torch.cuda.device(q.device):
-        o = torch.empty_like(q) if out is None else out
+        o = _like(q) if out is None else out
         _need(o, q, "out")
         if return_lse:
             if lse is None:
@@ -224,9 +239,9 @@ def na_bwd(q, k, v, o, d_o, lse, kernel_size, dilation=None, is_causal=None, sca
         _need(t, q, n)
     _need_lse(lse, q)
     with torch.cuda.device(q.device):
-        dq = torch.empty_like(q) if dq is None else dq
-        dk = torch.empty_like(q) if dk is None else dk
-        dv = torch.empty_like(q) if dv is None else dv
+        dq = _like(q) if dq is None else dq
+        dk = _like(q) if dk is None else dk
+        dv = _like(q) if dv is None else dv
         for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
             _need(t, q, n)
         need = na_bwd_workspace_size(p)
@@ -263,7 +278,7 @@ def na_tune(q, k, v, d_o, kernel_size, dilation=None, is_causal=None, scale=None
     _need_cuda(q)
     for t, n in ((k, "k"), (v, "v"), (d_o, "d_o")):
         _need(t, q, n)
-    o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
+    o, dq, dk, dv = (_like(q) for _ in range(4))
     lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
     ws = torch.empty((max(na_bwd_workspace_size(p), 16) + 3) // 4, dtype=torch.float32, device=q.device)
     c = (ctypes.c_int32 * 3)()

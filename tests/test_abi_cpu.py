@@ -80,10 +80,21 @@ def test_validation_codes(na, kw, status):
 
 
 def test_layout_and_impl_codes(na):
-    p = P(na)
-    arr = (ctypes.c_int64 * 6)(*range(6))
-    p.strides = ctypes.cast(arr, ctypes.c_void_p)
-    assert na.na_validate(p) == 11
+    def strided(st, **kw):
+        p = P(na, **kw)
+        p._arr = (ctypes.c_int64 * 6)(*st)
+        p.strides = ctypes.cast(p._arr, ctypes.c_void_p)
+        return na.na_validate(p)
+    assert strided(range(6)) == 11                                  # head_dim stride != 1
+    assert strided([16 * 64 * 2, 64, 2 * 64, 0, 0, 1], heads=2) == 0  # heads-last [B, X, H, D]
+    assert strided([0, 64, 64, 0, 0, 1]) == 11                       # a stride < 1
+    assert strided([1024, 68, 136, 0, 0, 1], heads=2) == 10         # 136 B rows: not 16-B multiples
+    assert strided([4096, 64, 256, 5, 0, 1], extent=[16]) == 0       # X1/X2 ignored beyond rank
+    # the binding passes a non-contiguous tensor's strides
+    x = torch.empty(2, 16, 4, 64, dtype=torch.float16).permute(0, 2, 1, 3)
+    p = na.na._problem_from(x, [3], None, None, None, "auto")
+    assert list(p._strides) == [16 * 4 * 64, 64, 4 * 64, 0, 0, 1]
+    assert na.na_validate(p) == 0
     p = P(na)
     p.impl = 7
     assert na.na_validate(p) == 14

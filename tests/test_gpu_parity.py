@@ -396,3 +396,58 @@ def test_context_parallel_slabs_match_oracle(na, ext, ker, dil, cau, D, dt, worl
         got = torch.cat(parts[n], dim=2).numpy()
         assert excess(got, ref.reshape(shp), dt) <= 0, (n, max_err(got, ref.reshape(shp)))
     assert max_err(torch.cat(parts["lse"], dim=2).numpy(), rlse.reshape(shp[:-1])) <= LSE_TOL[dt]
+
+
+# ------------------------------------------------- strided (non-contiguous) layouts
+
+STRIDED = [
+    # extent, kernel, dilation, causal, D, dtype, batch, impl, packed QKV
+    ([300], [33], [3], [0], 64, torch.float16, 2, "tc", False),
+    ([37, 20], [7, 5], [1, 2], [0, 0], 32, torch.bfloat16, 2, "tc", True),
+    ([6, 10, 13], [3, 5, 7], [1, 1, 1], [1, 0, 0], 128, torch.float16, 1, "tc", False),
+    ([12, 14, 9], [5, 5, 3], [1, 2, 1], [0, 0, 0], 64, torch.bfloat16, 3, "tc", True),
+    ([9, 16, 16], [3, 7, 7], [1, 1, 1], [1, 0, 0], 16, torch.float16, 2, "tc", False),
+    ([40], [7], [2], [1], 16, torch.float32, 2, "simt", False),
+    ([9, 11], [3, 5], [1, 1], [0, 1], 32, torch.float32, 2, "simt", True),
+    ([30, 44], [9, 13], [3, 2], [0, 1], 32, torch.float16, 2, "simt", False),
+]
+
+
+@pytest.mark.parametrize("ext,ker,dil,cau,D,dt,B,impl,packed", STRIDED)
+def test_strided_layouts(na, ext, ker, dil, cau, D, dt, B, impl, packed):
+    """Heads-last storage [B, X..., H, D] (or a packed [B, X..., 3, H, D] QKV
+    buffer) viewed as [B, H, X..., D]: the binding passes the strides, the
+    kernels address the rows through them (TMA tensor-map strides / strided
+    row offsets), batches whose stride does not merge with the heads' run as
+    separate sub-problems.  Same results as the oracle on contiguous copies."""
+    H = 3
+    cfg = na_synth.small_config(ext, ker, dil, cau, head_dim=D, batch=B, heads=H, dtype=dt)
+    q, k, v, do = na_synth.make_inputs(cfg, salt=23)
+    R = len(ext)
+    to_hl = (0, *range(2, 2 + R), 1, 2 + R)        # [B,H,X,D] -> [B,X,H,D]
+    from_hl = (0, 1 + R, *range(1, 1 + R), 2 + R)  # [B,X,H,D] -> [B,H,X,D]
+    if packed:
+        buf = torch.stack([t.permute(to_hl) for t in (q, k, v)], dim=1 + R).cuda()  # [B,X,3,H,D]
+        qs, ks, vs = (buf.select(1 + R, i).permute(from_hl) for i in range(3))
+    else:
+        qs, ks, vs = (t.permute(to_hl).contiguous().cuda().permute(from_hl) for t in (q, k, v))
+    dos = torch.empty_strided(qs.shape, qs.stride(), dtype=dt, device="cuda")
+    dos.copy_(do.cuda())
+    assert not qs.is_contiguous() and all(t.stride() == qs.stride() for t in (ks, vs, dos))
+    kw = dict(kernel_size=ker, dilation=dil, is_causal=[bool(c) for c in cau], impl=impl)
+    p = na.make_problem(B, H, ext, D, ker, dil, [bool(c) for c in cau], dtype=dt, impl=impl)
+    if impl == "tc" and na.na_selected_impl(p) != na.NA_IMPL_TC:
+        pytest.skip("problem outside the tensor-core path")
+    o, lse = na.na_fwd(qs, ks, vs, **kw)
+    dq, dk, dv = na.na_bwd(qs, ks, vs, o, dos, lse, **kw)
+    torch.cuda.synchronize()
+    assert o.stride() == qs.stride() and dq.stride() == qs.stride()
+    op = oracle_problem(cfg)
+    ro, rlse = oracle.fwd(op, q, k, v)
+    rdq, rdk, rdv = oracle.bwd(op, q, k, v, do, stored_o=False)
+    shp = (B, H, cfg.tokens, D)
+    got = [t.float().cpu().contiguous().reshape(shp) for t in (o, dq, dk, dv)]
+    assert excess(got[0], ro, dt) <= 0, max_err(got[0], ro)
+    assert max_err(lse.float().cpu().reshape(shp[:-1]), rlse) <= LSE_TOL[dt]
+    for g, r in zip(got[1:], (rdq, rdk, rdv)):
+        assert excess(g, r, dt) <= 0, max_err(g, r)
