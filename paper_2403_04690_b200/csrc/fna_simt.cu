@@ -72,17 +72,18 @@ __device__ __forceinline__ int token_of(const Geom& g, const Coord& co, const in
 // Element offset, inside its (b, h) slice, of the token at compacted
 // coordinates cc of co's residue class (Geom::sX strides; contiguous:
 // token_of * D).
-__device__ __forceinline__ long long elem_of(const Geom& g, const Coord& co, const int cc[3]) {
+__device__ __forceinline__ long long elem_of(const Geom& g, const Layout& ly, const Coord& co,
+                                             const int cc[3]) {
   long long e = 0;
 #pragma unroll
   for (int a = 0; a < 3; ++a)
-    if (a < g.rank) e += (long long)(co.r[a] + g.dil[a] * cc[a]) * g.sX[a];
+    if (a < g.rank) e += (long long)(co.r[a] + g.dil[a] * cc[a]) * ly.sX[a];
   return e;
 }
 
 // ------------------------------------------------------------------ forward
 template <typename T, int DPL>
-__global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict__ q,
+__global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, Layout ly, const T* __restrict__ q,
                                                     const T* __restrict__ k,
                                                     const T* __restrict__ v, T* __restrict__ o,
                                                     float* __restrict__ lse) {
@@ -90,9 +91,9 @@ __global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict_
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   const int bh = (int)(row / g.N), x = (int)(row % g.N);
-  const int64_t base = (int64_t)bh * g.sBH;
+  const int64_t base = (int64_t)bh * ly.sBH;
   const Coord co = decode(g, x);
-  const int64_t xe = base + elem_of(g, co, co.c);  // this query's row
+  const int64_t xe = base + elem_of(g, ly, co, co.c);  // this query's row
   float qr[DPL], acc[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict_
   for (cc[0] = lo[0]; cc[0] <= hi[0]; ++cc[0])
     for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
       for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
-        const int64_t y = base + elem_of(g, co, cc);
+        const int64_t y = base + elem_of(g, ly, co, cc);
         float s = 0.f;
 #pragma unroll
         for (int i = 0; i < DPL; ++i) {
@@ -141,14 +142,14 @@ __global__ void __launch_bounds__(256) fna_fwd_simt(Geom g, const T* __restrict_
 
 // ------------------------------------------------------------- bwd: D_x
 template <typename T>
-__global__ void __launch_bounds__(256) fna_bwd_pre(Geom g, const T* __restrict__ o,
+__global__ void __launch_bounds__(256) fna_bwd_pre(Geom g, Layout ly, const T* __restrict__ o,
                                                    const T* __restrict__ d_o,
                                                    float* __restrict__ Dvec) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   float s = 0.f;
-  const int64_t re = elem_of_token(g, (int)(row / g.N), (int)(row % g.N));
+  const int64_t re = elem_of_token(g, ly, (int)(row / g.N), (int)(row % g.N));
   for (int d = lane; d < g.D; d += 32) s = fmaf(ld(o + re + d), ld(d_o + re + d), s);
   s = warp_sum(s);
   if (lane == 0) Dvec[row] = s;
@@ -170,16 +171,16 @@ struct RvDiv {
 
 // Element offset of row `row` (= bh * N + token) in a Q/K/V/O-type tensor
 // (Geom::sBH / sX strides), with the same fast divisions.
-__device__ __forceinline__ long long row_elem(const Geom& g, const RvDiv& f, long long row) {
+__device__ __forceinline__ long long row_elem(const Geom& g, const Layout& ly, const RvDiv& f, long long row) {
   const uint32_t r32 = (uint32_t)row;
   const uint32_t bh = fdiv(r32, f.n);
   uint32_t n = r32 - bh * f.n.d;
-  long long off = (long long)bh * g.sBH;
+  long long off = (long long)bh * ly.sBH;
 #pragma unroll
   for (int a = 2; a >= 0; --a) {
     if (a < g.rank) {
       const uint32_t rest = fdiv(n, f.l[a]);
-      off += (long long)(n - rest * f.l[a].d) * g.sX[a];
+      off += (long long)(n - rest * f.l[a].d) * ly.sX[a];
       n = rest;
     }
   }
@@ -209,7 +210,7 @@ __device__ __forceinline__ long long rv_index(const Geom& g, const RvDiv& f, lon
 }
 
 template <typename T, int kPreRows>
-__global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restrict__ o,
+__global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, Layout ly, const T* __restrict__ o,
                                                        const T* __restrict__ d_o,
                                                        float* __restrict__ Dvec,
                                                        const float* __restrict__ lse, RvDiv f) {
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restri
       l[k] = lse[row];
       i[k] = rv_index(g, f, row);
     }
-    const long long re = g.contig ? row * g.D : (valid ? row_elem(g, f, row) : 0);
+    const long long re = ly.contig ? row * g.D : (valid ? row_elem(g, ly, f, row) : 0);
     a[k] = valid ? __ldg(reinterpret_cast<const uint4*>(o + re) + part) : make_uint4(0, 0, 0, 0);
     b[k] = valid ? __ldg(reinterpret_cast<const uint4*>(d_o + re) + part) : make_uint4(0, 0, 0, 0);
   }
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(256) fna_bwd_pre_vec(Geom g, const T* __restri
 
 // ------------------------------------------------------------- bwd: dQ
 template <typename T, int DPL>
-__global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__ q,
+__global__ void __launch_bounds__(256) fna_dq_simt(Geom g, Layout ly, const T* __restrict__ q,
                                                    const T* __restrict__ k,
                                                    const T* __restrict__ v,
                                                    const T* __restrict__ d_o,
@@ -282,9 +283,9 @@ __global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   const int bh = (int)(row / g.N), x = (int)(row % g.N);
-  const int64_t base = (int64_t)bh * g.sBH;
+  const int64_t base = (int64_t)bh * ly.sBH;
   const Coord co = decode(g, x);
-  const int64_t xe = base + elem_of(g, co, co.c);  // this query's row
+  const int64_t xe = base + elem_of(g, ly, co, co.c);  // this query's row
   float qr[DPL], dor[DPL], acc[DPL], pk[DPL];
   float csum = 0.f;
 #pragma unroll
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__
   for (cc[0] = lo[0]; cc[0] <= hi[0]; ++cc[0])
     for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
       for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
-        const int64_t y = base + elem_of(g, co, cc);
+        const int64_t y = base + elem_of(g, ly, co, cc);
         float s = 0.f, dp = 0.f;
 #pragma unroll
         for (int i = 0; i < DPL; ++i) {
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(256) fna_dq_simt(Geom g, const T* __restrict__
 
 // ------------------------------------------------------------- bwd: dK, dV
 template <typename T, int DPL>
-__global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, const T* __restrict__ q,
+__global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, Layout ly, const T* __restrict__ q,
                                                      const T* __restrict__ k,
                                                      const T* __restrict__ v,
                                                      const T* __restrict__ d_o,
@@ -351,9 +352,9 @@ __global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, const T* __restrict
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (int64_t)g.BH * g.N) return;
   const int bh = (int)(row / g.N), y = (int)(row % g.N);
-  const int64_t base = (int64_t)bh * g.sBH;
+  const int64_t base = (int64_t)bh * ly.sBH;
   const Coord co = decode(g, y);
-  const int64_t ye = base + elem_of(g, co, co.c);  // this key's row
+  const int64_t ye = base + elem_of(g, ly, co, co.c);  // this key's row
   float kr[DPL], vr[DPL], ak[DPL], av[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) {
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, const T* __restrict
     for (cc[1] = lo[1]; cc[1] <= hi[1]; ++cc[1])
       for (cc[2] = lo[2]; cc[2] <= hi[2]; ++cc[2]) {
         const int xt = token_of(g, co, cc);
-        const int64_t xo = base + elem_of(g, co, cc);
+        const int64_t xo = base + elem_of(g, ly, co, cc);
         float s = 0.f, dp = 0.f;
 #pragma unroll
         for (int i = 0; i < DPL; ++i) {
@@ -408,64 +409,64 @@ __global__ void __launch_bounds__(256) fna_dkdv_simt(Geom g, const T* __restrict
 }
 
 template <typename T, int DPL>
-cudaError_t launch_fwd(const Geom& g, const void* q, const void* k, const void* v, void* o,
+cudaError_t launch_fwd(const Geom& g, const Layout& ly, const void* q, const void* k, const void* v, void* o,
                        float* lse, cudaStream_t st) {
   const int64_t rows = (int64_t)g.BH * g.N;
   prof_begin(KID_FWD_SIMT, st);
   fna_fwd_simt<T, DPL><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      g, (const T*)q, (const T*)k, (const T*)v, (T*)o, lse);
+      g, ly, (const T*)q, (const T*)k, (const T*)v, (T*)o, lse);
   prof_end(st);
   return cudaGetLastError();
 }
 
 template <typename T, int DPL>
-cudaError_t launch_bwd(const Geom& g, const void* q, const void* k, const void* v, const void* o,
+cudaError_t launch_bwd(const Geom& g, const Layout& ly, const void* q, const void* k, const void* v, const void* o,
                        const void* d_o, const float* lse, void* dq, void* dk, void* dv,
                        float* Dvec, cudaStream_t st) {
   const int64_t rows = (int64_t)g.BH * g.N;
   const unsigned grid = (unsigned)((rows + 7) / 8);
   prof_begin(KID_BWD_PRE, st);
-  fna_bwd_pre<T><<<grid, 256, 0, st>>>(g, (const T*)o, (const T*)d_o, Dvec);
+  fna_bwd_pre<T><<<grid, 256, 0, st>>>(g, ly, (const T*)o, (const T*)d_o, Dvec);
   prof_end(st);
   // dQ first: for 16-bit inputs it corrects D_x in Dvec for dK/dV
   prof_begin(KID_DQ_SIMT, st);
-  fna_dq_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
+  fna_dq_simt<T, DPL><<<grid, 256, 0, st>>>(g, ly, (const T*)q, (const T*)k, (const T*)v,
                                             (const T*)d_o, lse, Dvec, (T*)dq);
   prof_end(st);
   prof_begin(KID_DKDV_SIMT, st);
-  fna_dkdv_simt<T, DPL><<<grid, 256, 0, st>>>(g, (const T*)q, (const T*)k, (const T*)v,
+  fna_dkdv_simt<T, DPL><<<grid, 256, 0, st>>>(g, ly, (const T*)q, (const T*)k, (const T*)v,
                                               (const T*)d_o, lse, Dvec, (T*)dk, (T*)dv);
   prof_end(st);
   return cudaGetLastError();
 }
 
 template <typename T>
-cudaError_t fwd_by_dim(const Geom& g, const void* q, const void* k, const void* v, void* o,
+cudaError_t fwd_by_dim(const Geom& g, const Layout& ly, const void* q, const void* k, const void* v, void* o,
                        float* lse, cudaStream_t st) {
-  if (g.D <= 32) return launch_fwd<T, 1>(g, q, k, v, o, lse, st);
-  if (g.D <= 64) return launch_fwd<T, 2>(g, q, k, v, o, lse, st);
-  if (g.D <= 128) return launch_fwd<T, 4>(g, q, k, v, o, lse, st);
-  return launch_fwd<T, 8>(g, q, k, v, o, lse, st);
+  if (g.D <= 32) return launch_fwd<T, 1>(g, ly, q, k, v, o, lse, st);
+  if (g.D <= 64) return launch_fwd<T, 2>(g, ly, q, k, v, o, lse, st);
+  if (g.D <= 128) return launch_fwd<T, 4>(g, ly, q, k, v, o, lse, st);
+  return launch_fwd<T, 8>(g, ly, q, k, v, o, lse, st);
 }
 
 template <typename T>
-cudaError_t bwd_by_dim(const Geom& g, const void* q, const void* k, const void* v, const void* o,
+cudaError_t bwd_by_dim(const Geom& g, const Layout& ly, const void* q, const void* k, const void* v, const void* o,
                        const void* d_o, const float* lse, void* dq, void* dk, void* dv,
                        float* Dvec, cudaStream_t st) {
-  if (g.D <= 32) return launch_bwd<T, 1>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
-  if (g.D <= 64) return launch_bwd<T, 2>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
-  if (g.D <= 128) return launch_bwd<T, 4>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
-  return launch_bwd<T, 8>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+  if (g.D <= 32) return launch_bwd<T, 1>(g, ly, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+  if (g.D <= 64) return launch_bwd<T, 2>(g, ly, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+  if (g.D <= 128) return launch_bwd<T, 4>(g, ly, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+  return launch_bwd<T, 8>(g, ly, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
 }
 
 }  // namespace
 
-cudaError_t simt_fwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+cudaError_t simt_fwd(int dtype, const Geom& g, const Layout& ly, const void* q, const void* k, const void* v,
                      void* o, float* lse, cudaStream_t st) {
   switch (dtype) {
-    case 0: return fwd_by_dim<float>(g, q, k, v, o, lse, st);
-    case 1: return fwd_by_dim<__half>(g, q, k, v, o, lse, st);
-    default: return fwd_by_dim<__nv_bfloat16>(g, q, k, v, o, lse, st);
+    case 0: return fwd_by_dim<float>(g, ly, q, k, v, o, lse, st);
+    case 1: return fwd_by_dim<__half>(g, ly, q, k, v, o, lse, st);
+    default: return fwd_by_dim<__nv_bfloat16>(g, ly, q, k, v, o, lse, st);
   }
 }
 
@@ -476,7 +477,7 @@ cudaError_t rv_clear_padding(const Geom& g, float* Dvec, cudaStream_t st) {
   return cudaMemsetAsync(Dvec, 0, (size_t)g.BH * g.nres * 2 * g.rv_plane * sizeof(float), st);
 }
 
-cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, const float* lse,
+cudaError_t bwd_preprocess(int dtype, const Geom& g, const Layout& ly, const void* o, const void* d_o, const float* lse,
                            float* Dvec, cudaStream_t st) {
   const int64_t rows = (int64_t)g.BH * g.N;
   const unsigned grid = (unsigned)((rows + 7) / 8);
@@ -498,30 +499,30 @@ cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* 
   const int rpt = g.rank == 1 ? 2 : 1;  // rows per thread
   const unsigned vgrid = (unsigned)((rows * (g.D / 8) + 256 * rpt - 1) / (256 * rpt));
   switch (dtype) {
-    case 0: fna_bwd_pre<float><<<grid, 256, 0, st>>>(g, (const float*)o, (const float*)d_o, Dvec); break;
+    case 0: fna_bwd_pre<float><<<grid, 256, 0, st>>>(g, ly, (const float*)o, (const float*)d_o, Dvec); break;
     case 1:
-      if (rpt == 2) fna_bwd_pre_vec<__half, 2><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec, lse, f);
-      else fna_bwd_pre_vec<__half, 1><<<vgrid, 256, 0, st>>>(g, (const __half*)o, (const __half*)d_o, Dvec, lse, f);
+      if (rpt == 2) fna_bwd_pre_vec<__half, 2><<<vgrid, 256, 0, st>>>(g, ly, (const __half*)o, (const __half*)d_o, Dvec, lse, f);
+      else fna_bwd_pre_vec<__half, 1><<<vgrid, 256, 0, st>>>(g, ly, (const __half*)o, (const __half*)d_o, Dvec, lse, f);
       break;
     default:
       if (rpt == 2)
-        fna_bwd_pre_vec<__nv_bfloat16, 2><<<vgrid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
+        fna_bwd_pre_vec<__nv_bfloat16, 2><<<vgrid, 256, 0, st>>>(g, ly, (const __nv_bfloat16*)o,
                                                                  (const __nv_bfloat16*)d_o, Dvec, lse, f);
       else
-        fna_bwd_pre_vec<__nv_bfloat16, 1><<<vgrid, 256, 0, st>>>(g, (const __nv_bfloat16*)o,
+        fna_bwd_pre_vec<__nv_bfloat16, 1><<<vgrid, 256, 0, st>>>(g, ly, (const __nv_bfloat16*)o,
                                                                  (const __nv_bfloat16*)d_o, Dvec, lse, f);
   }
   prof_end(st);
   return cudaGetLastError();
 }
 
-cudaError_t simt_bwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+cudaError_t simt_bwd(int dtype, const Geom& g, const Layout& ly, const void* q, const void* k, const void* v,
                      const void* o, const void* d_o, const float* lse, void* dq, void* dk,
                      void* dv, float* Dvec, cudaStream_t st) {
   switch (dtype) {
-    case 0: return bwd_by_dim<float>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
-    case 1: return bwd_by_dim<__half>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
-    default: return bwd_by_dim<__nv_bfloat16>(g, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+    case 0: return bwd_by_dim<float>(g, ly, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+    case 1: return bwd_by_dim<__half>(g, ly, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
+    default: return bwd_by_dim<__nv_bfloat16>(g, ly, q, k, v, o, d_o, lse, dq, dk, dv, Dvec, st);
   }
 }
 

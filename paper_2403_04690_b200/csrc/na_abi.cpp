@@ -112,17 +112,6 @@ na::Geom make_geom(const na_problem* p) {
     s *= g.L[a];
   }
   for (int a = p->rank; a < 3; ++a) g.tstride[a] = 1;
-  for (int a = 0; a < 3; ++a) g.sX[a] = a < p->rank ? (long long)g.tstride[a] * g.D : 0;
-  g.sBH = (long long)n * g.D;
-  g.contig = 1;
-  if (p->strides) {
-    g.contig = 0;
-    for (int a = 0; a < p->rank; ++a) g.sX[a] = p->strides[2 + a];
-    // B and H merge into one slice index when stride_B = H * stride_H; the
-    // ABI calls split other layouts into one launch set per batch entry
-    // (split_batches), each with B = 1, where sBH = stride_H.
-    g.sBH = p->heads > 1 ? p->strides[1] : p->strides[0];
-  }
   g.scale = p->scale > 0.f ? p->scale : 1.f / std::sqrt((float)p->head_dim);
   g.scale_log2 = g.scale * 1.4426950408889634f;
   g.nres = 1;
@@ -138,6 +127,23 @@ na::Geom make_geom(const na_problem* p) {
   }
   g.rv_plane = cs;
   return g;
+}
+
+// Element strides of the Q/K/V/O-type tensors (na_geom.cuh, Layout).
+na::Layout make_layout(const na_problem* p, const na::Geom& g) {
+  na::Layout ly{};
+  for (int a = 0; a < 3; ++a) ly.sX[a] = a < p->rank ? (long long)g.tstride[a] * g.D : 0;
+  ly.sBH = (long long)g.N * g.D;
+  ly.contig = 1;
+  if (p->strides) {
+    ly.contig = 0;
+    for (int a = 0; a < p->rank; ++a) ly.sX[a] = p->strides[2 + a];
+    // B and H merge into one slice index when stride_B = H * stride_H; the
+    // ABI calls split other layouts into one launch set per batch entry
+    // (split_batches), each with B = 1, where sBH = stride_H.
+    ly.sBH = p->heads > 1 ? p->strides[1] : p->strides[0];
+  }
+  return ly;
 }
 
 // Backward workspace: the SIMT path's D_x vector [BH*N] or the tensor-core
@@ -271,6 +277,7 @@ na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* 
                 "CUDA-core kernels explicitly)", why);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int launches = 1, total = 0;
+  const na::Layout ly = make_layout(p, g);
   const int nb = split_batches(p) ? p->batch : 1;
   if (nb > 1) g.BH = p->heads;
   const int esz = p->dtype == NA_F32 ? 4 : 2;
@@ -280,8 +287,8 @@ na_status na_fwd(const na_problem* p, const void* q, const void* k, const void* 
     const void *qb = adv(q, eo, esz), *kb = adv(k, eo, esz), *vb = adv(v, eo, esz);
     void* ob = adv(o, eo, esz);
     float* lb = lse ? lse + (long long)b * (nb > 1 ? (long long)g.BH * g.N : 0) : nullptr;
-    e = impl == NA_IMPL_TC ? na::tc_fwd((int)p->dtype, g, qb, kb, vb, ob, lb, st, &launches)
-                           : na::simt_fwd((int)p->dtype, g, qb, kb, vb, ob, lb, st);
+    e = impl == NA_IMPL_TC ? na::tc_fwd((int)p->dtype, g, ly, qb, kb, vb, ob, lb, st, &launches)
+                           : na::simt_fwd((int)p->dtype, g, ly, qb, kb, vb, ob, lb, st);
     total += launches;
   }
   launches = total;
@@ -320,6 +327,7 @@ na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* 
                 "CUDA-core kernels explicitly)", why);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int launches = 3, total = 0;
+  const na::Layout ly = make_layout(p, g);
   const int nb = split_batches(p) ? p->batch : 1;
   if (nb > 1) g.BH = p->heads;
   const int esz = p->dtype == NA_F32 ? 4 : 2;
@@ -328,10 +336,10 @@ na_status na_bwd(const na_problem* p, const void* q, const void* k, const void* 
     const long long eo = (long long)b * (nb > 1 ? p->strides[0] : 0);
     const float* lb = lse + (long long)b * (nb > 1 ? (long long)g.BH * g.N : 0);
     e = impl == NA_IMPL_TC
-            ? na::tc_bwd((int)p->dtype, g, adv(q, eo, esz), adv(k, eo, esz), adv(v, eo, esz), adv(o, eo, esz),
+            ? na::tc_bwd((int)p->dtype, g, ly, adv(q, eo, esz), adv(k, eo, esz), adv(v, eo, esz), adv(o, eo, esz),
                          adv(d_o, eo, esz), lb, adv(dq, eo, esz), adv(dk, eo, esz), adv(dv, eo, esz),
                          (float*)workspace, st, &launches)
-            : na::simt_bwd((int)p->dtype, g, adv(q, eo, esz), adv(k, eo, esz), adv(v, eo, esz),
+            : na::simt_bwd((int)p->dtype, g, ly, adv(q, eo, esz), adv(k, eo, esz), adv(v, eo, esz),
                            adv(o, eo, esz), adv(d_o, eo, esz), lb, adv(dq, eo, esz), adv(dk, eo, esz),
                            adv(dv, eo, esz), (float*)workspace, st);
     total += launches;

@@ -62,12 +62,6 @@ struct Geom {
   int D;           // head dim
   int L[3], k[3], dil[3], causal[3];  // padded with (1, 1, 1, 0) beyond rank
   int tstride[3];  // token stride of each axis in the flat spatial index
-  // Element strides of the 16-bit / fp32 tensors (head_dim stride 1): from
-  // one (b, h) slice to the next, and per spatial axis (padded with 0).
-  // Contiguous [B,H,X...,D]: sBH = N*D, sX[a] = tstride[a]*D.  LSE, the
-  // row vectors and the workspace are always contiguous.
-  long long sBH, sX[3];
-  int contig;  // 1: the contiguous layout (sBH = N*D, sX[a] = tstride[a]*D)
   float scale;     // softmax scale
   float scale_log2;  // scale * log2(e)
   // Backward row-vector layout (tensor-core path): per (b,h) and residue
@@ -80,11 +74,23 @@ struct Geom {
   long long rv_plane;  // elements per plane = rv_cs[0] * rv_lc[0]
 };
 
+// Element strides of the Q/K/V/O-type tensors (head_dim stride 1): from one
+// (b, h) slice to the next, and per spatial axis (0 beyond rank).
+// Contiguous [B,H,X...,D]: sBH = N*D, sX[a] = tstride[a]*D.  LSE, the row
+// vectors and the workspace are always contiguous.  Kept out of Geom: the
+// tensor-core kernels never read strides (their TMA tensor maps carry them),
+// and growing their by-value Geom parameter measurably changed their
+// register allocation (dK/dV spills, +9-15 %).
+struct Layout {
+  long long sBH, sX[3];
+  int contig;  // 1: the contiguous layout
+};
+
 // Element offset of flat token `tok` of slice `bh` in a Q/K/V/O-type tensor
 // (the token's coordinate on axis a is (tok / tstride[a]) % L[a]).
-NA_HD long long elem_of_token(const Geom& g, int bh, int tok) {
-  long long off = (long long)bh * g.sBH;
-  for (int a = 0; a < g.rank; ++a) off += (long long)((tok / g.tstride[a]) % g.L[a]) * g.sX[a];
+NA_HD long long elem_of_token(const Geom& g, const Layout& ly, int bh, int tok) {
+  long long off = (long long)bh * ly.sBH;
+  for (int a = 0; a < g.rank; ++a) off += (long long)((tok / g.tstride[a]) % g.L[a]) * ly.sX[a];
   return off;
 }
 

@@ -23,9 +23,9 @@ void prof_begin(int kernel_id, cudaStream_t st);
 void prof_end(cudaStream_t st);
 
 // dtype: 0 = fp32, 1 = fp16, 2 = bf16 (matches na_dtype)
-cudaError_t simt_fwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+cudaError_t simt_fwd(int dtype, const Geom& g, const Layout& ly, const void* q, const void* k, const void* v,
                      void* o, float* lse, cudaStream_t st);
-cudaError_t simt_bwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+cudaError_t simt_bwd(int dtype, const Geom& g, const Layout& ly, const void* q, const void* k, const void* v,
                      const void* o, const void* d_o, const float* lse, void* dq, void* dk,
                      void* dv, float* Dvec, cudaStream_t st);
 
@@ -35,7 +35,7 @@ cudaError_t simt_bwd(int dtype, const Geom& g, const void* q, const void* k, con
 // Zero the row-vector layout's padding slots (ragged residue classes) before
 // the tensor-core backward writes the rest.
 cudaError_t rv_clear_padding(const Geom& g, float* Dvec, cudaStream_t st);
-cudaError_t bwd_preprocess(int dtype, const Geom& g, const void* o, const void* d_o, const float* lse,
+cudaError_t bwd_preprocess(int dtype, const Geom& g, const Layout& ly, const void* o, const void* d_o, const float* lse,
                            float* Dvec, cudaStream_t st);
 
 // tcgen05 path.  tc_supported() is a pure host check; the launchers return
@@ -68,9 +68,9 @@ void set_plan_choice(const Geom& g, int dtype, PlanChoice c);
 // times candidates with it, so the process-wide table never holds a
 // transient pick.
 void set_plan_override(const PlanChoice* c);
-cudaError_t tc_fwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+cudaError_t tc_fwd(int dtype, const Geom& g, const Layout& ly, const void* q, const void* k, const void* v,
                    void* o, float* lse, cudaStream_t st, int* launches);
-cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+cudaError_t tc_bwd(int dtype, const Geom& g, const Layout& ly, const void* q, const void* k, const void* v,
                    const void* o, const void* d_o, const float* lse, void* dq, void* dk,
                    void* dv, float* Dvec, cudaStream_t st, int* launches);
 

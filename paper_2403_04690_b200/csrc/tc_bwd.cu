@@ -937,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // are encoded by the caller) happens before the first launch, so an error
 // leaves the stream and the workspace untouched (include/na.h).
 template <int RANK, int D, bool BF16, bool PRECISE = false>
-cudaError_t launch_all(int dtype, const Geom& g, const TcPlan* pls, const BwdMaps& mkv, const BwdMaps& mq,
+cudaError_t launch_all(int dtype, const Geom& g, const Layout& ly, const TcPlan* pls, const BwdMaps& mkv, const BwdMaps& mq,
                        const void* o, const void* d_o, float* rv, const float* lse, cudaStream_t st) {
   constexpr bool kFuse = RANK == 1 && D <= 64;  // dQ forms the row vectors (see bwd_body)
   const int smem_kv = BwdSmem<D, true, false>::kBytes + 1024;
@@ -955,7 +955,7 @@ cudaError_t launch_all(int dtype, const Geom& g, const TcPlan* pls, const BwdMap
   // Row-vector layout: rank 1, written by the dQ kernel (fused preprocess;
   // slots no token maps to, ragged residue classes, must read as 0);
   // otherwise by the preprocess kernel.
-  e = kFuse ? rv_clear_padding(g, rv, st) : bwd_preprocess(dtype, g, o, d_o, lse, rv, st);
+  e = kFuse ? rv_clear_padding(g, rv, st) : bwd_preprocess(dtype, g, ly, o, d_o, lse, rv, st);
   if (e != cudaSuccess) return e;
   // dQ first: when fused it also writes the row vectors (-LSE*log2(e), D)
   // the dK/dV kernel streams.
@@ -971,31 +971,31 @@ cudaError_t launch_all(int dtype, const Geom& g, const TcPlan* pls, const BwdMap
 }
 
 template <int RANK>
-cudaError_t by_type(int dtype, const Geom& g, const TcPlan* pl, const BwdMaps& mkv, const BwdMaps& mq,
+cudaError_t by_type(int dtype, const Geom& g, const Layout& ly, const TcPlan* pl, const BwdMaps& mkv, const BwdMaps& mq,
                     const void* o, const void* d_o, float* rv, const float* lse, cudaStream_t st) {
   if (dtype == 2) {
     const bool pr = bf16_precise(g);
     if (g.D == 128)
-      return pr ? launch_all<RANK, 128, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
-                : launch_all<RANK, 128, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+      return pr ? launch_all<RANK, 128, true, true>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st)
+                : launch_all<RANK, 128, true>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st);
     if (g.D == 64)
-      return pr ? launch_all<RANK, 64, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
-                : launch_all<RANK, 64, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+      return pr ? launch_all<RANK, 64, true, true>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st)
+                : launch_all<RANK, 64, true>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st);
     if (g.D == 16)
-      return pr ? launch_all<RANK, 16, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
-                : launch_all<RANK, 16, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
-    return pr ? launch_all<RANK, 32, true, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st)
-              : launch_all<RANK, 32, true>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+      return pr ? launch_all<RANK, 16, true, true>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st)
+                : launch_all<RANK, 16, true>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st);
+    return pr ? launch_all<RANK, 32, true, true>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st)
+              : launch_all<RANK, 32, true>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st);
   }
-  if (g.D == 128) return launch_all<RANK, 128, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
-  if (g.D == 64) return launch_all<RANK, 64, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
-  if (g.D == 16) return launch_all<RANK, 16, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
-  return launch_all<RANK, 32, false>(dtype, g, pl, mkv, mq, o, d_o, rv, lse, st);
+  if (g.D == 128) return launch_all<RANK, 128, false>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st);
+  if (g.D == 64) return launch_all<RANK, 64, false>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st);
+  if (g.D == 16) return launch_all<RANK, 16, false>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st);
+  return launch_all<RANK, 32, false>(dtype, g, ly, pl, mkv, mq, o, d_o, rv, lse, st);
 }
 
 }  // namespace
 
-cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const void* v,
+cudaError_t tc_bwd(int dtype, const Geom& g, const Layout& ly, const void* q, const void* k, const void* v,
                    const void* o, const void* d_o, const float* lse, void* dq, void* dk, void* dv,
                    float* Dvec, cudaStream_t st, int* launches) {
   const char* why;
@@ -1012,22 +1012,22 @@ cudaError_t tc_bwd(int dtype, const Geom& g, const void* q, const void* k, const
   cudaError_t e;
   for (int w = 0; w < 2; ++w) {
     const TcPlan& pl = pls[w];
-    if ((e = make_map(&mm[w]->a0, dtype, g, tile_src[w][0], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
-    if ((e = make_map(&mm[w]->a1, dtype, g, tile_src[w][1], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
-    if ((e = make_map(&mm[w]->b0, dtype, g, chunk_src[w][0], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
-    if ((e = make_map(&mm[w]->b1, dtype, g, chunk_src[w][1], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+    if ((e = make_map(&mm[w]->a0, dtype, g, ly, tile_src[w][0], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+    if ((e = make_map(&mm[w]->a1, dtype, g, ly, tile_src[w][1], pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+    if ((e = make_map(&mm[w]->b0, dtype, g, ly, chunk_src[w][0], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+    if ((e = make_map(&mm[w]->b1, dtype, g, ly, chunk_src[w][1], pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
   }
-  if ((e = make_map(&mkv.out0, dtype, g, dk, pls[0].tq, pls[0].q_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&mkv.out1, dtype, g, dv, pls[0].tq, pls[0].q_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&mq.out0, dtype, g, dq, pls[1].tq, pls[1].q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mkv.out0, dtype, g, ly, dk, pls[0].tq, pls[0].q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mkv.out1, dtype, g, ly, dv, pls[0].tq, pls[0].q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mq.out0, dtype, g, ly, dq, pls[1].tq, pls[1].q_box_x)) != cudaSuccess) return e;
   mq.out1 = mq.out0;
-  if ((e = make_map(&mq.o, dtype, g, o, pls[1].tq, pls[1].q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&mq.o, dtype, g, ly, o, pls[1].tq, pls[1].q_box_x)) != cudaSuccess) return e;
   mkv.o = mq.o;
   *launches = (g.rank == 1 && g.D <= 64) ? 2 : 3;  // rank 1: preprocess fused into dQ (head_dim <= 64)
   switch (g.rank) {
-    case 1: return by_type<1>(dtype, g, pls, mkv, mq, o, d_o, Dvec, lse, st);
-    case 2: return by_type<2>(dtype, g, pls, mkv, mq, o, d_o, Dvec, lse, st);
-    default: return by_type<3>(dtype, g, pls, mkv, mq, o, d_o, Dvec, lse, st);
+    case 1: return by_type<1>(dtype, g, ly, pls, mkv, mq, o, d_o, Dvec, lse, st);
+    case 2: return by_type<2>(dtype, g, ly, pls, mkv, mq, o, d_o, Dvec, lse, st);
+    default: return by_type<3>(dtype, g, ly, pls, mkv, mq, o, d_o, Dvec, lse, st);
   }
 }
 

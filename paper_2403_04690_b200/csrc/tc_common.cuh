@@ -19,7 +19,7 @@ namespace na {
 TcPlan make_plan(const Geom& g, int tile_rows, int pick = 0, int* ncand = nullptr);
 // (plan_choice / set_plan_choice: na_kernels.h)
 int num_sms();  // SMs of the current device (cached per device)
-cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base,
+cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const Layout& ly, const void* base,
                      const int box[3], int box_x);
 
 template <bool BF16>

@@ -559,17 +559,17 @@ cudaError_t by_type(int dtype, const Geom& g, const TcPlan& pl, const FwdMaps& m
 
 }  // namespace
 
-cudaError_t tc_fwd(int dtype, const Geom& g, const void* q, const void* k, const void* v, void* o,
+cudaError_t tc_fwd(int dtype, const Geom& g, const Layout& ly, const void* q, const void* k, const void* v, void* o,
                    float* lse, cudaStream_t st, int* launches) {
   const char* why;
   if (!tc_supported(dtype, g, &why)) return cudaErrorNotSupported;
   TcPlan pl = make_plan(g, /*q_tile_rows=*/128, plan_choice(g, dtype).fwd);
   FwdMaps maps;
   cudaError_t e;
-  if ((e = make_map(&maps.q, dtype, g, q, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&maps.k, dtype, g, k, pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&maps.v, dtype, g, v, pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
-  if ((e = make_map(&maps.o, dtype, g, o, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&maps.q, dtype, g, ly, q, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&maps.k, dtype, g, ly, k, pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&maps.v, dtype, g, ly, v, pl.ckv, pl.kv_box_x)) != cudaSuccess) return e;
+  if ((e = make_map(&maps.o, dtype, g, ly, o, pl.tq, pl.q_box_x)) != cudaSuccess) return e;
   *launches = 1;
   switch (g.rank) {
     case 1: return by_type<1>(dtype, g, pl, maps, lse, st);

@@ -400,7 +400,7 @@ EncodeTiled encoder() {
 // walked with elementStrides = dilation so one box covers one residue class.
 namespace {
 
-cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* base, const int box[3],
+cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const Layout& ly, const void* base, const int box[3],
                        int box_x) {
   EncodeTiled enc = encoder();
   if (!enc) return cudaErrorNotSupported;
@@ -413,13 +413,13 @@ cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* b
   for (int i = 1; i <= R; ++i) {
     const int a = R - i;
     dims[i] = g.L[a];
-    strides[i - 1] = (cuuint64_t)g.sX[a] * 2;  // element strides (contiguous: tstride * D)
+    strides[i - 1] = (cuuint64_t)ly.sX[a] * 2;  // element strides (contiguous: tstride * D)
     const int b = (i == 1) ? box_x : box[a];
     boxd[i] = (cuuint32_t)(b * g.dil[a]);
     estr[i] = g.dil[a];
   }
   dims[R + 1] = g.BH;
-  strides[R] = (cuuint64_t)g.sBH * 2;
+  strides[R] = (cuuint64_t)ly.sBH * 2;
   boxd[R + 1] = 1;
   estr[R + 1] = 1;
   const CUtensorMapSwizzle sw = g.D >= 64   ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -438,7 +438,7 @@ cudaError_t encode_map(CUtensorMap* map, int dtype, const Geom& g, const void* b
 // reads (base pointer, dtype, geometry, box): a map holds only an address
 // and a geometry, so a hit is exactly the map encoding would produce, and a
 // steady-state call (same buffers) encodes nothing.
-cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* base, const int box[3],
+cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const Layout& ly, const void* base, const int box[3],
                      int box_x) {
   struct Entry {
     long long key[18];
@@ -449,13 +449,13 @@ cudaError_t make_map(CUtensorMap* map, int dtype, const Geom& g, const void* bas
   thread_local Entry cache[kEntries];
   thread_local int used = 0, next = 0;
   const long long key[18] = {dtype, g.rank, g.D, g.BH, box_x, g.L[0], g.L[1], g.L[2], g.dil[0], g.dil[1], g.dil[2],
-                       box[0], box[1], box[2], g.sBH, g.sX[0], g.sX[1], g.sX[2]};
+                       box[0], box[1], box[2], ly.sBH, ly.sX[0], ly.sX[1], ly.sX[2]};
   for (int i = 0; i < used; ++i)
     if (cache[i].base == base && std::equal(key, key + 18, cache[i].key)) {
       *map = cache[i].map;
       return cudaSuccess;
     }
-  const cudaError_t e = encode_map(map, dtype, g, base, box, box_x);
+  const cudaError_t e = encode_map(map, dtype, g, ly, base, box, box_x);
   if (e != cudaSuccess) return e;
   Entry& en = cache[next];
   next = (next + 1) % kEntries;
