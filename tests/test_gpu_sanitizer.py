@@ -1,5 +1,5 @@
 """compute-sanitizer over tiny launches of every kernel family and
-instantiation class (tools/run_small.py: 1-D/2-D/3-D, fp16/bf16/fp32, D 32/64,
+instantiation class (tools/run_small.py: 1-D/2-D/3-D, fp16/bf16 (both variants)/fp32, D 16-128, small-tile forward, strided layouts,
 tensor-core and CUDA-core paths): memcheck (out-of-bounds / misaligned
 accesses), racecheck (shared-memory hazards across the hand-written mbarrier
 and TMEM pipelines), synccheck (illegal barrier use) and initcheck (reads of
