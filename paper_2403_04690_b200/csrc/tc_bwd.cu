@@ -82,13 +82,18 @@ struct BwdSmem {
   static constexpr int kTile = kHalves * kAHalf;      // stationary tile
   static constexpr int kBHalf = kBRows * kRowBytes;
   static constexpr int kBTile = kHalves * kBHalf;     // streamed tile
-  static constexpr int kA = 0;                        // stationary [2 bufs][2 tiles] (K,V | Q,dO)
-  static constexpr int kO = kA + 4 * kTile;           // fused dQ: stationary O tile [2 bufs]
-  static constexpr int kB0 = kO + (FUSE ? 2 * kTile : 0);  // streamed [kSt] (Q | K)
+  // Stationary buffers: head_dim <= 32 tiles are small (8 KB) and short
+  // (C configs: one or two sub-chunks), so four buffers let the producer
+  // load a tile's stationary pair three tiles ahead instead of waiting for
+  // the store of the tile two back (whose latency was exposed per tile).
+  static constexpr int kAB = D <= 32 ? 4 : 2;
+  static constexpr int kA = 0;                        // stationary [kAB bufs][2 tiles] (K,V | Q,dO)
+  static constexpr int kO = kA + 2 * kAB * kTile;     // fused dQ: stationary O tile [kAB bufs]
+  static constexpr int kB0 = kO + (FUSE ? kAB * kTile : 0);  // streamed [kSt] (Q | K)
   static constexpr int kB1 = kB0 + kSt * kBTile;      // streamed [kSt] (dO | V)
   static constexpr int kVec = kB1 + kSt * kBTile;     // [kSt][-LSE2 x128 | D x128] fp32 (dK/dV)
   static constexpr int kBar = kVec + (KV ? kSt * 256 * 4 : 0);
-  static constexpr int kDx = kBar + 256;              // exact-D dQ: [2 groups][128] fp32 partials
+  static constexpr int kDx = kBar + 512;              // (barriers + TMEM slot words) exact-D dQ: [2 groups][128] fp32 partials
   static constexpr int kBytes = kDx + (EXACT ? 2 * 128 * 4 : 0);
 };
 
@@ -110,9 +115,9 @@ struct BwdTmem {
 };
 
 enum : int {
-  B_AF = 0,                 // stationary tiles full [2]
-  B_AE = B_AF + 2,          // stationary tiles empty [2] (the TMA-store issuer, after the read)
-  B_B = B_AE + 2,           // streamed stage full [kStages]
+  B_AF = 0,                 // stationary tiles full [kAB <= 4]
+  B_AE = B_AF + 4,          // stationary tiles empty [kAB] (the TMA-store issuer, after the read)
+  B_B = B_AE + 4,           // streamed stage full [kStages]
   B_E = B_B + kStages,      // streamed stage empty [kStages]
   B_S = B_E + kStages,      // S and dP of a sub-chunk ready [3] (TMEM buffer gu % 3)
   B_P = B_S + 3,            // P / dS written in place over that buffer [3] (128 arrivals)
@@ -180,9 +185,11 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
 
   if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < S::kAB; ++b) {
       ptx::mbar_init(bar + B_AF + b, 1);
       ptx::mbar_init(bar + B_AE + b, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(bar + B_OF + b, 1);
       ptx::mbar_init(bar + B_OE + b, KV_STATIONARY ? 128 : kCompute);
     }
@@ -237,8 +244,9 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     for (unsigned tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       TileCtx<RANK> t;
       if (!t.init(g, pl, tile, /*inverse=*/KV_STATIONARY)) continue;
-      const int ab = ti & 1;
-      if (ti >= 2) ptx::mbar_wait(bar + B_AE + ab, ((ti >> 1) - 1) & 1);
+      constexpr int kAB = S::kAB;
+      const int ab = ti % kAB;
+      if (ti >= kAB) ptx::mbar_wait(bar + B_AE + ab, ((ti / kAB) - 1) & 1);
       if (NA_BWD_TRACE_ON) NA_TRACE_EV(0, tr, 1);
       uint8_t* a0 = smem + S::kA + (2 * ab) * S::kTile;
       uint8_t* a1 = a0 + S::kTile;
@@ -330,7 +338,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       TileCtx<RANK> ct;
       for (unsigned tile = seek_tile<RANK, KV_STATIONARY>(g, pl, blockIdx.x, num_tiles, ct); tile < num_tiles;
            tile = seek_tile<RANK, KV_STATIONARY>(g, pl, tile + gridDim.x, num_tiles, ct)) {
-        const int ab = c_ti & 1;
+        const int ab = c_ti % S::kAB;
         const uint32_t a0 = ptx::smem_u32(smem + S::kA + (2 * ab) * S::kTile);
         const uint32_t a1 = a0 + S::kTile;
         const int nsub = ct.nchunks * ns;
@@ -339,7 +347,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
           const int h = c_u % ns, s = kv % kStages;
           const uint32_t b3 = gu % kNB, r3 = gu / kNB;
           if (gu >= kNB) ptx::mbar_wait(bar + B_PE + b3, (r3 - 1) & 1);  // buffer's previous OUT done
-          if (c_u == 0) ptx::mbar_wait(bar + B_AF + ab, (c_ti >> 1) & 1);
+          if (c_u == 0) ptx::mbar_wait(bar + B_AF + ab, (c_ti / S::kAB) & 1);
           if (h == 0) ptx::mbar_wait(bar + B_B + s, (kv / kStages) & 1);
           ptx::tc_fence_after();
           const uint32_t off = h * 64 * S::kRowBytes;
@@ -468,8 +476,8 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     };
     auto row_vals = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r, uint32_t tix, float lse_v,
                         float& nl2, float& d) {
-      const int ab = tix & 1;
-      ptx::mbar_wait(bar + B_AF + ab, (tix >> 1) & 1);
+      const int ab = tix % S::kAB;
+      ptx::mbar_wait(bar + B_AF + ab, (tix / S::kAB) & 1);
       const uint8_t* ot = smem + S::kO + ab * S::kTile;
       const uint8_t* dt = smem + S::kA + (2 * ab + 1) * S::kTile;
       float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // two packed-FMA chains
@@ -619,7 +627,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
       return i;
     };
     auto epilogue = [&](const TileCtx<RANK>& t, uint32_t tix) {
-      const int ob = kOutDouble ? (tix & 1) : 0, ab = tix & 1;
+      const int ob = kOutDouble ? (tix & 1) : 0, ab = tix % S::kAB;
       ptx::mbar_wait(bar + B_OF + ob, kOutDouble ? ((tix >> 1) & 1) : (tix & 1));
       if (tracer) NA_TRACE_EV(2 + grp, tr, 24);
       ptx::tc_fence_after();
