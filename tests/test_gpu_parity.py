@@ -451,3 +451,37 @@ def test_strided_layouts(na, ext, ker, dil, cau, D, dt, B, impl, packed):
     assert max_err(lse.float().cpu().reshape(shp[:-1]), rlse) <= LSE_TOL[dt]
     for g, r in zip(got[1:], (rdq, rdk, rdv)):
         assert excess(g, r, dt) <= 0, max_err(g, r)
+
+
+# ------------------------------------------- bf16 variant rule (R13)
+
+BF16_RULE = [
+    # extent, kernel, causal, expected na_bf16_precise
+    ([600], [127], [0], 1),
+    ([600], [129], [0], 0),
+    ([44, 40], [11, 11], [0, 0], 1),
+    ([44, 40], [13, 11], [0, 0], 0),
+    ([10, 24, 24], [3, 7, 7], [0, 0, 0], 0),
+    ([10, 24, 24], [3, 7, 7], [1, 0, 0], 1),
+]
+
+
+@pytest.mark.parametrize("ext,ker,cau,precise", BF16_RULE)
+@pytest.mark.parametrize("D", [32, 64])
+def test_bf16_variant_rule_boundary(na, ext, ker, cau, precise, D):
+    """Both bf16 kernel variants meet the bound on either side of the
+    128-key rule (the plain one just above it, the precise one just below)."""
+    dt = torch.bfloat16
+    cfg = na_synth.small_config(ext, ker, [1] * len(ext), cau, head_dim=D, batch=1, heads=2, dtype=dt)
+    p = na.make_problem(1, 2, list(ext), D, ker, [1] * len(ext), [bool(c) for c in cau], dtype=dt)
+    assert na.na_bf16_precise(p) == precise
+    q, k, v, do = na_synth.make_inputs(cfg, salt=29)
+    o, lse, dq, dk, dv = run_gpu(na, cfg, q, k, v, do, "tc")
+    op = oracle_problem(cfg)
+    ro, rlse = oracle.fwd(op, q, k, v)
+    rdq, rdk, rdv = oracle.bwd(op, q, k, v, do, stored_o=False)
+    shp = (1, 2, cfg.tokens, D)
+    assert excess(o.reshape(shp), ro, dt) <= 0, max_err(o.reshape(shp), ro)
+    assert max_err(lse.reshape(shp[:-1]), rlse) <= LSE_TOL[dt]
+    for g, r in ((dq, rdq), (dk, rdk), (dv, rdv)):
+        assert excess(g.reshape(shp), r, dt) <= 0, max_err(g.reshape(shp), r)
