@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT)
 import na_synth  # noqa: E402
 import paper_2403_04690_b200.na as nab  # noqa: E402
 
-nab.LIB_PATH = os.path.join(ROOT, "paper_2403_04690_b200", "libna_trace.so")
+nab.LIB_PATH = os.environ.get("NA_TRACE_LIB", os.path.join(ROOT, "paper_2403_04690_b200", "libna_trace.so"))
 L = nab.lib()
 L.na_debug_set_trace_bwd.argtypes = [ctypes.c_void_p, ctypes.c_int]
 which = int(sys.argv[2]) if len(sys.argv) > 2 else 1
