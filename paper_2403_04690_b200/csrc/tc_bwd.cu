@@ -461,7 +461,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
     // the separate preprocess pass over O and dO.  Otherwise: read from the
     // row-vector layout the preprocess kernel wrote.
     auto row_lse = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r) {
-      return r.valid ? lse[r.out_offset(g, t) / g.D] : 0.f;
+      return r.valid ? lse[r.token_index(g, t)] : 0.f;
     };
     auto row_read = [&](const TileCtx<RANK>& t, const RowCtx<RANK>& r, float& nl2, float& d) {
       nl2 = 0.f;

@@ -270,12 +270,16 @@ struct RowCtx {
     }
   }
 
-  // Element offset of this row's token in a [BH, N, D] tensor.
-  __device__ __forceinline__ long long out_offset(const Geom& g, const TileCtx<RANK>& t) const {
+  // Index of this row's token in a [BH, N] row vector (LSE).
+  __device__ __forceinline__ long long token_index(const Geom& g, const TileCtx<RANK>& t) const {
     long long tok = 0;
 #pragma unroll
     for (int a = 0; a < RANK; ++a) tok += (long long)(t.r[a] + g.dil[a] * c[a]) * g.tstride[a];
-    return ((long long)t.bh * g.N + tok) * g.D;
+    return (long long)t.bh * g.N + tok;
+  }
+  // Element offset of this row's token in a [BH, N, D] tensor.
+  __device__ __forceinline__ long long out_offset(const Geom& g, const TileCtx<RANK>& t) const {
+    return token_index(g, t) * g.D;
   }
 
   // Validity bitmask of the <=128 chunk columns for this row: column

@@ -494,10 +494,7 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
         ptx::bulk_wait_read<0>();
         ptx::mbar_arrive(bar + B_QE + qb);  // Q buffer reusable
       }
-      if (lse && r.valid) {
-        const long long ooff = r.out_offset(g, t);
-        lse[ooff / g.D] = (m_ref + __log2f(l)) * 0.69314718055994531f;
-      }
+      if (lse && r.valid) lse[r.token_index(g, t)] = (m_ref + __log2f(l)) * 0.69314718055994531f;
       ++ti;
     }
     if (threadIdx.x == 0) ptx::bulk_wait<0>();  // all O stores complete before exit

@@ -485,3 +485,33 @@ def test_bf16_variant_rule_boundary(na, ext, ker, cau, precise, D):
     assert max_err(lse.reshape(shp[:-1]), rlse) <= LSE_TOL[dt]
     for g, r in ((dq, rdq), (dk, rdk), (dv, rdv)):
         assert excess(g.reshape(shp), r, dt) <= 0, max_err(g.reshape(shp), r)
+
+
+@pytest.mark.parametrize("ext,ker,dil,cau,D,dt", [
+    ([300], [33], [2], [1], 64, torch.float16),
+    ([20, 27], [7, 5], [2, 1], [0, 0], 32, torch.bfloat16),
+    ([6, 10, 12], [3, 5, 5], [1, 1, 2], [1, 0, 0], 64, torch.float16),
+])
+def test_slice_view_calls_are_bitwise_the_whole_call(na, ext, ker, dil, cau, D, dt):
+    """The multi-GPU strong split and bench.py's pipelined e2e both call the
+    library on views of a range of flattened (b,h) slices ([1, n, X..., D]
+    sub-blocks of the contiguous tensors).  Each (b,h) slice is an
+    independent problem, so the slices' outputs must not depend
+    on which other slices share the launch: bitwise equal to the whole call."""
+    cfg = na_synth.small_config(ext, ker, dil, cau, head_dim=D, dtype=dt, batch=2, heads=3)
+    q, k, v, do = (t.cuda() for t in na_synth.make_inputs(cfg, salt=7))
+    kw = dict(kernel_size=ker, dilation=dil, is_causal=[bool(c) for c in cau])
+    o, lse = na.na_fwd(q, k, v, **kw)
+    dq, dk, dv = na.na_bwd(q, k, v, o, do, lse, **kw)
+    n = cfg.batch * cfg.heads
+    flat = lambda t: t.reshape(1, n, *t.shape[2:])  # noqa: E731
+    qf, kf, vf, dof = (flat(t) for t in (q, k, v, do))
+    outs = [torch.empty_like(flat(t)) for t in (o, lse, dq, dk, dv)]
+    for a, b in ((0, 1), (1, 4), (4, 6)):
+        sl = (qf[:, a:b], kf[:, a:b], vf[:, a:b])
+        na.na_fwd(*sl, out=outs[0][:, a:b], lse=outs[1][:, a:b], **kw)
+        na.na_bwd(*sl, outs[0][:, a:b], dof[:, a:b], outs[1][:, a:b],
+                  dq=outs[2][:, a:b], dk=outs[3][:, a:b], dv=outs[4][:, a:b], **kw)
+    torch.cuda.synchronize()
+    for name, whole, part in zip(("O", "LSE", "dQ", "dK", "dV"), (o, lse, dq, dk, dv), outs):
+        assert torch.equal(flat(whole), part), name

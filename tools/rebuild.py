@@ -19,6 +19,9 @@ if "--out" in args:
     del args[i:i + 2]
 srcs = b.sources()
 deps = max(os.path.getmtime(d) for d in b._deps() if not d.endswith((".cu", ".cpp")))
+# named sources compile into a directory of their own (parallel variant builds)
+vdir = b.BUILD if out == b.OUT else os.path.join(b.BUILD, "v_" + os.path.basename(out))
+os.makedirs(vdir, exist_ok=True)
 objs = []
 for s in srcs:
     obj = os.path.join(b.BUILD, os.path.basename(s) + ".o")
@@ -26,7 +29,7 @@ for s in srcs:
         not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(s), deps))
     if want:
         print("compile", os.path.basename(s), flush=True)
-        b._compile(s, False)
+        obj = b._compile(s, False, vdir)
     objs.append(obj)
 cmd = [b.NVCC, *b.ARCH, "-shared", "-o", out, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
 subprocess.run(cmd, check=True)

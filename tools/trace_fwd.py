@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT)
 import na_synth  # noqa: E402
 import paper_2403_04690_b200.na as nab  # noqa: E402
 
-nab.LIB_PATH = os.path.join(ROOT, "paper_2403_04690_b200", "libna_trace.so")
+nab.LIB_PATH = os.environ.get("NA_TRACE_LIB", os.path.join(ROOT, "paper_2403_04690_b200", "libna_trace.so"))
 L = nab.lib()
 L.na_debug_set_trace_fwd.argtypes = [ctypes.c_void_p]
 
@@ -43,7 +43,7 @@ print(f"{name}: forward {ev0.elapsed_time(ev1):.3f} ms")
 t = buf.view(64, 4, 256).cpu()
 for cta in (0, 1, 37):
     evs = []
-    for role in range(3):
+    for role in range(4):
         for x in t[cta, role].tolist():
             if x == 0:
                 break
