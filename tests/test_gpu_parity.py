@@ -66,6 +66,13 @@ SMALL = [
     ([12, 16, 16], [5, 3, 3], [1, 1, 1], [1, 0, 0]),
     ([10, 20, 24], [3, 5, 5], [1, 2, 1], [0, 0, 0]),
     ([30, 44], [9, 13], [3, 2], [0, 1]),
+    # small residue classes with an even innermost dilation (C_d8's 7x7
+    # classes; causal on either axis; unequal classes on the outer axis; 3-D)
+    ([56, 56], [7, 7], [8, 8], [0, 0]),
+    ([16, 24], [3, 5], [2, 4], [0, 0]),
+    ([14, 14], [7, 3], [2, 2], [0, 1]),
+    ([13, 20], [5, 5], [2, 4], [1, 0]),
+    ([2, 6, 20], [2, 3, 5], [1, 2, 4], [1, 0, 0]),
 ]
 
 
