@@ -25,8 +25,10 @@ os.makedirs(vdir, exist_ok=True)
 objs = []
 for s in srcs:
     obj = os.path.join(b.BUILD, os.path.basename(s) + ".o")
-    want = (os.path.basename(s) in args) if args else (
-        not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(s), deps))
+    # a named source, or any source whose in-tree object predates a header
+    # (objects built against another struct layout must not be mixed)
+    stale = not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(s), deps)
+    want = (os.path.basename(s) in args or os.path.getmtime(obj) < deps) if args else stale
     if want:
         print("compile", os.path.basename(s), flush=True)
         obj = b._compile(s, False, vdir)
