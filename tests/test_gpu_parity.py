@@ -339,7 +339,13 @@ def _random_cases(n=24, seed=2024, dims=(16, 32, 64)):
     return out
 
 
-@pytest.mark.parametrize("ext,ker,dil,cau,D,dt", _random_cases(64) + _random_cases(24, seed=128, dims=(128,)))
+# NA_RANDOM_EXTRA=n adds n more seeded cases (head_dim 16-128) for one-off
+# extended sweeps (profiles/r02_random_sweep.txt); 0 in the default suite.
+_EXTRA = int(__import__("os").environ.get("NA_RANDOM_EXTRA", "0"))
+
+
+@pytest.mark.parametrize("ext,ker,dil,cau,D,dt", _random_cases(64) + _random_cases(24, seed=128, dims=(128,)) +
+                         (_random_cases(_EXTRA, seed=777, dims=(16, 32, 64, 128)) if _EXTRA else []))
 def test_random_problems_match_oracle(na, ext, ker, dil, cau, D, dt):
     """Seeded random shapes, windows, dilations, causal mixes, head dims and
     dtypes on the tensor-core path (planner, masks, halos, ragged classes)."""
