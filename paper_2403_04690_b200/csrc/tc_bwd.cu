@@ -781,7 +781,7 @@ __device__ __forceinline__ void bwd_body(const BwdMaps& maps, const Geom& g, con
               x1.y = (ww >> (c + 3)) & 1u ? x1.y : -INFINITY;
             }
             p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
-            p1 = use_poly(c) ? exp2_poly2(x1)                   // FMA pipe
+            p1 = use_poly<KV_STATIONARY ? (RANK == 3 ? 1 : 0) : (D <= 32 ? 3 : 1)>(c) ? exp2_poly2(x1)                   // FMA pipe
                              : make_float2(ptx::ex2(x1.x), ptx::ex2(x1.y));
             ds0 = __fmul2_rn(p0, __fadd2_rn(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])),
                                             make_float2(-dd4.x, -dd4.y)));

@@ -74,17 +74,23 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(p.x) + ex), __int_as_float(__float_as_int(p.y) + ey));
 }
 
-// Which exponentials go to the FMA-pipe polynomial: the element pair at
-// column c (c % 4 == 2 within each group of 4).  The softmax loops are
-// issue-bound as well as MUFU-bound, and the polynomial costs ~6 issue slots
-// per element against ~1 for MUFU, so only part of the elements take it.
-// NA_POLY_MODE: 0 none, 1 one pair in four groups-of-two (25%), 2 every
-// second pair (50%).
-#ifndef NA_POLY_MODE
-#define NA_POLY_MODE 1
-#endif
+// Which exponentials go to the FMA-pipe polynomial: at column c of a
+// 4-column step (c = 0, 4, ..., 28 within a 32-column group) the step's
+// second pair.  Mode 0: none; 1: steps with c & 4 (25 % of the elements);
+// 2: every step (50 %); 3: c & 12 == 4 (12.5 %).  The polynomial costs ~6
+// issue slots per element against ~1 for MUFU, so the best share depends
+// on how MUFU- vs issue-bound a kernel is: measured per kernel and rank
+// (round 2, session 3) -- forward rank 1: 1, rank
+// 2/3: 0; dK/dV rank 1/2: 0, rank 3: 1; dQ: 1, head_dim <= 32: 3.
+// NA_POLY_MODE (build flag) overrides every kernel's choice.
+template <int MODE>
 __device__ __forceinline__ constexpr bool use_poly(int c) {
-  return NA_POLY_MODE == 2 ? true : (NA_POLY_MODE == 1 ? (c & 4) != 0 : false);
+#ifdef NA_POLY_MODE
+  constexpr int m = NA_POLY_MODE;
+#else
+  constexpr int m = MODE;
+#endif
+  return m == 2 ? true : m == 1 ? (c & 4) != 0 : m == 3 ? (c & 12) == 4 : false;
 }
 
 // Which (b*h, residue class, tile) a CTA owns, and the tile's halo.

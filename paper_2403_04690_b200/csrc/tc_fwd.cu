@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<SMALL>::kCtas)
             const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(s4[2]), __uint_as_float(s4[3])),
                                          make_float2(sl2, sl2), make_float2(nmu, nmu));
             const float2 p0 = make_float2(ptx::ex2(x0.x), ptx::ex2(x0.y));  // MUFU
-            const float2 p1 = use_poly(c) ? exp2_poly2(x1)                   // FMA pipe
+            const float2 p1 = use_poly<RANK == 1 ? 1 : 0>(c) ? exp2_poly2(x1)                   // FMA pipe
                                           : make_float2(ptx::ex2(x1.x), ptx::ex2(x1.y));
             acc0 = __fadd2_rn(acc0, p0);
             acc1 = __fadd2_rn(acc1, p1);
